@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark: TabNet predict+explain rows/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config hr]
+                    [--precision tf32x3] [--impl ours|reference]
+
+One "step" = one fused forward of the workload's batch (HR: 65,536 rows,
+BASELINE.json configs[1]) with inputs resident in HBM.  Multi-GPU (torchrun, one
+process per GPU): each rank processes its own batch of rows — independent row
+shards, no collective on the data path — so scaling is "weak"; timing is
+CUDA events on the launching stream, max over ranks.  Rank 0 prints ONE JSON line.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port under oracle/, bitwise equal to the reference's apply) on the
+host's cores with a process pool, on the same config/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2510_19689_b200 import workloads as W  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="hr", choices=sorted(W.WORKLOADS))
+    ap.add_argument("--rows", type=int, default=0, help="rows per rank (default: the config's batch)")
+    ap.add_argument("--precision", default="tf32x3")
+    ap.add_argument("--regime", default="trained", choices=["trained", "init"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--latency-sweep", action="store_true",
+                    help="also report p50/p99 device+e2e latency for batches 1..1024 (config 3)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def nearest_rank(vals, q):
+    """Nearest-rank percentile (reference telemetry/metrics.py:33-37)."""
+    s = sorted(vals)
+    if not s:
+        return None
+    k = max(1, int(np.ceil(q / 100.0 * len(s))))
+    return s[k - 1]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=1)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- cpu arm
+def _oracle_worker(args):
+    name, regime, start, rows = args
+    from oracle import tabnet_oracle as O
+    w = W.WORKLOADS[name]
+    m = W.make_model(name, regime)
+    x = W.make_inputs(w, rows, start=start).astype(np.float64)
+    t0 = time.perf_counter()
+    O.apply_model(m, x)
+    return time.perf_counter() - t0
+
+
+class CpuReference:
+    """The reference algorithm on host cores: oracle/tabnet_oracle.py (bitwise
+    equal to tabserve TabNetModel.apply) over a fork pool of contiguous row shards
+    (its einsum path is single-threaded)."""
+
+    def __init__(self, name: str, regime: str, rows_per_step: int):
+        import multiprocessing as mp
+        self.procs = max(1, len(os.sched_getaffinity(0)))
+        self.name, self.regime = name, regime
+        self.rows = rows_per_step
+        self.pool = mp.get_context("fork").Pool(self.procs)
+
+    def step(self) -> float:
+        bounds = np.linspace(0, self.rows, self.procs + 1).astype(int)
+        jobs = [(self.name, self.regime, int(a), int(b - a)) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        # the shards run concurrently: a step lasts as long as its slowest shard
+        return max(self.pool.map(_oracle_worker, jobs))
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_rows_per_step(w: W.Workload, procs: int) -> int:
+    per_core = {"adult": 16384, "hr": 4096, "hr_latency": 4096, "bls": 1536, "wide": 96}[w.name]
+    return int(min(w.batch, per_core * procs))
+
+
+def run_reference(a) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w = W.WORKLOADS[a.config]
+    procs = max(1, len(os.sched_getaffinity(0)))
+    rows = cpu_rows_per_step(w, procs)
+    ref = CpuReference(a.config, a.regime, rows)
+    for _ in range(a.warmup):
+        ref.step()
+    times = [ref.step() for _ in range(a.steps)]
+    ref.close()
+    total = sum(times)
+    value = rows * a.steps / total
+    line = {
+        "impl": "reference", "metric": "TabNet inferences/sec (predict+explain)",
+        "value": value, "unit": "rows/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.description, "rows_per_step": rows, "regime": a.regime},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": "port",
+                         "sample": f"{rows} rows/step of {a.config} ({a.regime} weights), "
+                                   f"oracle/tabnet_oracle.py over {procs} fork-pool processes"},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def profile_traffic(config: str, precision: str):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        e = d.get(f"{config}/{precision}")
+        return e.get("dram_bytes_per_launch") if e else None
+    except Exception:
+        return None
+
+
+def run_ours(a) -> None:
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2510_19689_b200 import _native as N
+    from paper_2510_19689_b200.device import DeviceRunner
+    from paper_2510_19689_b200.network import TabNetModel
+
+    w = W.WORKLOADS[a.config]
+    rows = a.rows or w.batch
+    counts = W.algorithmic_counts(w)
+    model = TabNetModel.from_reference(W.make_model(a.config, a.regime), precision=a.precision,
+                                       device=local)
+    runner = DeviceRunner(model, rows, device=local)
+    f = w.feature_count
+    # rotating input/output sets so the timed region always streams from HBM
+    per_set = rows * counts["bytes_per_row"]
+    nsets = max(2, int(np.ceil(2.5 * L2_BYTES / per_set)))
+    nsets = min(nsets, 8)
+    xs = [torch.from_numpy(W.make_inputs(w, rows, start=(rank * nsets + i) * rows)).to(dev)
+          for i in range(nsets)]
+    outs = [runner.alloc_outputs(rows) for _ in range(nsets)]
+    stream = torch.cuda.current_stream(dev)
+
+    for i in range(a.warmup):
+        runner.run(xs[i % nsets], outs[i % nsets])
+    torch.cuda.synchronize()
+    runner.check_finite()
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    ev[0].record(stream)
+    for i in range(a.steps):
+        runner.run(xs[i % nsets], outs[i % nsets])
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    per_step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max = float(t.item())
+    value = world * rows * a.steps / (total_ms_max / 1e3)
+    kernel_ms = total_ms / a.steps     # one launch per step: kernel-only device time
+
+    # ---- end to end through the C-ABI host call: pinned host in/out, H2D+D2H timed
+    e2e = None
+    if not a.no_e2e:
+        xh = torch.from_numpy(W.make_inputs(w, rows, start=rank * rows)).pin_memory()
+        oh = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in runner.outputs.items()}
+        np_out = {k: v.numpy() for k, v in oh.items()}
+        xnp = xh.numpy()
+        eng = model.engine(device=local)
+        for _ in range(max(2, a.warmup // 2)):
+            eng.forward_host_f32(xnp, 0, np_out)
+        e2e_steps = max(5, min(a.steps, 30))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eng.forward_host_f32(xnp, 0, np_out)
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = rows * f * 4
+        d2h = sum(v.numel() * v.element_size() for v in oh.values())
+        e2e = {"value": world * rows * e2e_steps / float(te.item()), "unit": "rows/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": 1e3 * float(te.item()) / e2e_steps,
+               "path": "tbn_forward_host (C-ABI, pinned host fp32 buffers, 3-stream chunked H2D/kernel/D2H)"}
+
+    # ---- latency sweep (config 3) ----
+    latency = None
+    if a.latency_sweep and rank == 0:
+        latency = latency_sweep(model, local, f)
+
+    # ---- CPU baseline (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        procs = max(1, len(os.sched_getaffinity(0)))
+        crow = cpu_rows_per_step(w, procs)
+        ref = CpuReference(a.config, a.regime, crow)
+        ref.step()
+        ct = [ref.step() for _ in range(3)]
+        ref.close()
+        cpu = {"value": crow * 3 / sum(ct), "unit": "rows/s", "cores": procs, "kind": "port",
+               "sample": f"{crow} rows x 3 steps of {a.config} ({a.regime} weights), "
+                         f"oracle/tabnet_oracle.py (bitwise = reference apply) on {procs} processes"}
+
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = counts["bytes_per_row"] * rows / (kernel_ms / 1e3) / 1e9
+    tflops = counts["flops_per_row"] * rows / (kernel_ms / 1e3) / 1e12
+    traffic = profile_traffic(a.config, a.precision)
+    if rank == 0:
+        line = {
+            "metric": "TabNet inferences/sec (predict+explain)",
+            "value": value, "unit": "rows/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": total_ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": {"tf32x3": "fp32 (3xTF32 tcgen05 GEMMs)", "tf32": "tf32",
+                                           "bf16": "bf16", "fp32": "fp32 (CUDA-core FFMA)"}[a.precision],
+            "data": "synthetic",
+            "config": {"workload": w.description, "rows_per_rank": rows, "regime": a.regime,
+                       "precision": a.precision, "outputs": "logits, probabilities, masks (S,B,F), importance, class",
+                       "parallelism": f"row-shard x{world} (no collective)",
+                       "l2": f"rotating {nsets} input/output sets = {nsets * per_set / 2**20:.0f} MiB > 126 MiB L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "algorithmic_bytes_per_row": counts["bytes_per_row"],
+                         "algorithmic_flops_per_row": counts["flops_per_row"],
+                         "tensor_tflops_at_algorithmic_flops": tflops,
+                         "kernel_ms_per_launch": kernel_ms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+            "latency_ms": {"p50": nearest_rank(per_step_ms, 50), "p99": nearest_rank(per_step_ms, 99),
+                           "batch": rows, "kind": "device (CUDA events), per batch"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": a.steps,
+            "clocks": clk,
+        }
+        if latency is not None:
+            line["latency_sweep"] = latency
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def latency_sweep(model, local, f):
+    """HR shape, batches 1..1024 (BASELINE config 3): nearest-rank p50/p99 of the
+    device-only kernel time and of the end-to-end host call."""
+    import torch
+    from paper_2510_19689_b200.device import DeviceRunner
+    res = {}
+    eng = model.engine(device=local)
+    runner = DeviceRunner(model, 1024, device=local)
+    stream = torch.cuda.current_stream()
+    w = W.WORKLOADS["hr_latency"]
+    for b in (1, 4, 16, 64, 256, 1024):
+        x = torch.from_numpy(W.make_inputs(w, b)).cuda()
+        for _ in range(20):
+            runner.run(x)
+        torch.cuda.synchronize()
+        dev_ms = []
+        for _ in range(300):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            runner.run(x)
+            e1.record(stream)
+            e1.synchronize()
+            dev_ms.append(e0.elapsed_time(e1))
+        xh = torch.from_numpy(W.make_inputs(w, b)).pin_memory()
+        oh = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in runner.views(b).items()}
+        np_out = {k: v.numpy() for k, v in oh.items()}
+        e2e_ms = []
+        for i in range(320):
+            t0 = time.perf_counter()
+            eng.forward_host_f32(xh.numpy(), 0, np_out)
+            if i >= 20:
+                e2e_ms.append(1e3 * (time.perf_counter() - t0))
+        res[str(b)] = {"device_p50": nearest_rank(dev_ms, 50), "device_p99": nearest_rank(dev_ms, 99),
+                       "e2e_p50": nearest_rank(e2e_ms, 50), "e2e_p99": nearest_rank(e2e_ms, 99)}
+    return res
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

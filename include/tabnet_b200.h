@@ -1,0 +1,141 @@
+/*
+ * tabnet_b200.h — C ABI of libtabnet_b200.so, the B200 (sm_100a) engine for
+ * TabNet batch predict + feature-mask explain.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   /root/reference/pkg/src/tabserve/model/network.py:195-267  TabNetModel.apply
+ *   /root/reference/pkg/src/tabserve/model/network.py:269-281  TabNetModel.forward
+ *   /root/reference/pkg/src/tabserve/model/sparsemax.py:13-41  sparsemax
+ *   /root/reference/pkg/src/tabserve/model/io.py:22-36         crc32c (.tbnt trailer)
+ * The reference is pure Python/NumPy and has no FFI of its own; these entry
+ * points are what a ctypes binding inside tabserve.model would call
+ * (INTEGRATION.md shows that stub).  No torch types cross this boundary: plain
+ * pointers, sizes and an opaque cudaStream_t passed as void*.
+ *
+ * Error convention (errors.py:4-41): every call returns a tbn_status; the
+ * Python shim maps TBN_ERR_INVALID_INPUT -> InvalidInputError,
+ * TBN_ERR_CONFIG -> ConfigurationError, TBN_ERR_CUDA/UNSUPPORTED -> DeviceError.
+ * tbn_last_error() gives the thread-local message of the last failure.
+ */
+#ifndef TABNET_B200_H
+#define TABNET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TBN_ABI_VERSION 1
+
+typedef enum {
+  TBN_OK = 0,
+  TBN_ERR_INVALID_INPUT = 1, /* width mismatch, non-finite feature, rows < 1   (network.py:207-211) */
+  TBN_ERR_CONFIG = 2,        /* inconsistent config / params                   (config.py:29-41, network.py:110-114) */
+  TBN_ERR_CUDA = 3,          /* CUDA runtime failure or no device                                         */
+  TBN_ERR_UNSUPPORTED = 4    /* shape outside the compiled kernel instances                               */
+} tbn_status;
+
+/* Arithmetic of the FC contractions.  Everything else (GLU, sparsemax, prior,
+ * aggregation, softmax) is fp32 on CUDA cores in every mode. */
+typedef enum {
+  TBN_PREC_TF32X3 = 0, /* tcgen05 kind::tf32, hi/lo split, 3 MMAs: fp32-faithful (parity mode, default) */
+  TBN_PREC_TF32 = 1,   /* tcgen05 kind::tf32, 1 MMA                                                   */
+  TBN_PREC_BF16 = 2,   /* tcgen05 kind::f16 (bf16 operands), 1 MMA                                    */
+  TBN_PREC_FP32 = 3    /* CUDA-core fp32 FFMA kernel (no tensor cores; reference-precision check)     */
+} tbn_precision;
+
+/* apply() flags (network.py:195-196) */
+#define TBN_FLAG_NORMALIZED 1u      /* input is already normalized: skip the frozen affine        */
+#define TBN_FLAG_BATCH_STATS 2u     /* negative control: normalize with this batch's mean/var     */
+
+typedef struct {
+  int32_t feature_count; /* F            (config.py:20)  */
+  int32_t n_classes;     /* C >= 2       (config.py:21)  */
+  int32_t n_d;           /* decision width               */
+  int32_t n_a;           /* attention width              */
+  int32_t n_steps;       /* S                            */
+  int32_t reserved;
+  double gamma;          /* prior relaxation (config.py:26) */
+} tbn_config;
+
+/* Output views; any pointer may be NULL to skip that output.
+ *   logits, probabilities : (rows, C) row-major float32
+ *   masks                 : (S, rows, F) step-major float32  (network.py:231)
+ *   importance            : (rows, F) float32
+ *   predicted_class       : (rows,) int32, argmax with lowest-index ties */
+typedef struct {
+  float* logits;
+  float* probabilities;
+  float* masks;
+  float* importance;
+  int32_t* predicted_class;
+} tbn_outputs;
+
+typedef struct {
+  double* logits;
+  double* probabilities;
+  double* masks;
+  double* importance;
+  int32_t* predicted_class;
+} tbn_outputs_f64;
+
+typedef struct tbn_model tbn_model;
+
+/* Library identity. */
+int32_t tbn_abi_version(void);
+const char* tbn_last_error(void);                   /* thread-local, never NULL */
+int32_t tbn_device_count(void);                     /* 0 when no CUDA device is usable */
+
+/* Build a device-resident model from the reference's params dict
+ * (network.py:71-97 names and shapes, row-major float64, used as x @ W) and
+ * frozen normalization stats (network.py:104-107).  n_params entries of
+ * (names[i], values[i], sizes[i] = element count).  Packs weights once for the
+ * chosen precision (K0) and uploads them to `device`. */
+tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,
+                            const double* const* values, const int64_t* sizes,
+                            int32_t n_params, const double* norm_mean,
+                            const double* norm_var, int32_t precision,
+                            int32_t device, tbn_model** out);
+void tbn_model_destroy(tbn_model* model);
+tbn_status tbn_model_info(const tbn_model* model, tbn_config* cfg,
+                          int32_t* precision, int32_t* device);
+
+/* Device workspace needed by tbn_forward for `rows` rows (>= 256 bytes). */
+size_t tbn_workspace_bytes(const tbn_model* model, int64_t rows, uint32_t flags);
+
+/* Async forward on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * x: device float32 (rows, F) row-major.  Outputs are device pointers.
+ * A non-finite input sets *err_flag (device int32, may be NULL) to nonzero;
+ * the caller checks it after synchronizing (tbn_forward_host does).
+ * Per-row results are bitwise independent of `rows`, tile position, grid size
+ * and concurrency (invariance.py:56-82). */
+tbn_status tbn_forward(const tbn_model* model, const float* x, int64_t rows,
+                       uint32_t flags, const tbn_outputs* out, int32_t* err_flag,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Synchronous host-buffer forward (the reference-facing call): stages x
+ * through pinned memory on a per-thread stream, runs tbn_forward, copies the
+ * outputs back, and returns TBN_ERR_INVALID_INPUT on non-finite input.
+ * Reentrant: safe from many host threads at once. */
+tbn_status tbn_forward_host(const tbn_model* model, const float* x, int64_t rows,
+                            uint32_t flags, const tbn_outputs* out);
+/* Same with the reference's float64 arrays on both sides (numpy apply path). */
+tbn_status tbn_forward_host_f64(const tbn_model* model, const double* x, int64_t rows,
+                                uint32_t flags, const tbn_outputs_f64* out);
+
+/* Row-wise sparsemax on device (sparsemax.py:13-41): z, out (rows, n) fp32. */
+tbn_status tbn_sparsemax(const float* z, int64_t rows, int32_t n, float* out,
+                         void* stream);
+/* Host-buffer sparsemax (float64 in/out, computed on device in fp32). */
+tbn_status tbn_sparsemax_host_f64(const double* z, int64_t rows, int32_t n, double* out);
+
+/* CRC-32C (Castagnoli, reflected 0x82F63B78) as io.py:22-36, hardware
+ * accelerated on the host CPU when SSE4.2 is present.  Pure host code. */
+uint32_t tbn_crc32c(const uint8_t* data, size_t n, uint32_t crc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TABNET_B200_H */

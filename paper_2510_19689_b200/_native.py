@@ -1,0 +1,127 @@
+"""ctypes binding of libtabnet_b200.so (include/tabnet_b200.h).
+
+Loading never needs a GPU; compute entry points fail with DeviceError when no
+CUDA device is usable (there is no CPU fallback anywhere in the product path).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import ConfigurationError, DeviceError, InvalidInputError, TabserveError
+
+LIB_PATH = Path(__file__).resolve().parent / "libtabnet_b200.so"
+
+TBN_OK, TBN_ERR_INVALID_INPUT, TBN_ERR_CONFIG, TBN_ERR_CUDA, TBN_ERR_UNSUPPORTED = range(5)
+PREC_TF32X3, PREC_TF32, PREC_BF16, PREC_FP32 = range(4)
+PRECISIONS = {"tf32x3": PREC_TF32X3, "tf32": PREC_TF32, "bf16": PREC_BF16, "fp32": PREC_FP32}
+FLAG_NORMALIZED = 1
+FLAG_BATCH_STATS = 2
+
+# Every symbol include/tabnet_b200.h declares (tests check the .so exports them).
+EXPORTED = (
+    "tbn_abi_version", "tbn_last_error", "tbn_device_count", "tbn_model_create",
+    "tbn_model_destroy", "tbn_model_info", "tbn_workspace_bytes", "tbn_forward",
+    "tbn_forward_host", "tbn_forward_host_f64", "tbn_sparsemax",
+    "tbn_sparsemax_host_f64", "tbn_crc32c",
+)
+
+
+class TbnConfig(C.Structure):
+    _fields_ = [("feature_count", C.c_int32), ("n_classes", C.c_int32), ("n_d", C.c_int32),
+                ("n_a", C.c_int32), ("n_steps", C.c_int32), ("reserved", C.c_int32),
+                ("gamma", C.c_double)]
+
+
+class TbnOutputs(C.Structure):
+    _fields_ = [("logits", C.c_void_p), ("probabilities", C.c_void_p), ("masks", C.c_void_p),
+                ("importance", C.c_void_p), ("predicted_class", C.c_void_p)]
+
+
+TbnOutputsF64 = TbnOutputs   # same layout (pointers)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """Load (once) and return the engine library; raises DeviceError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise DeviceError(f"{LIB_PATH.name} is not built (run __graft_entry__.build() or "
+                              f"python -m paper_2510_19689_b200.build); no CPU fallback exists")
+        L = C.CDLL(str(LIB_PATH))
+        vp, i32, i64, u32, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_size_t
+        L.tbn_abi_version.restype = i32
+        L.tbn_last_error.restype = C.c_char_p
+        L.tbn_device_count.restype = i32
+        L.tbn_model_create.restype = i32
+        L.tbn_model_create.argtypes = [C.POINTER(TbnConfig), C.POINTER(C.c_char_p),
+                                       C.POINTER(C.c_void_p), C.POINTER(C.c_int64), i32,
+                                       vp, vp, i32, i32, C.POINTER(vp)]
+        L.tbn_model_destroy.restype = None
+        L.tbn_model_destroy.argtypes = [vp]
+        L.tbn_model_info.restype = i32
+        L.tbn_model_info.argtypes = [vp, C.POINTER(TbnConfig), C.POINTER(i32), C.POINTER(i32)]
+        L.tbn_workspace_bytes.restype = sz
+        L.tbn_workspace_bytes.argtypes = [vp, i64, u32]
+        L.tbn_forward.restype = i32
+        L.tbn_forward.argtypes = [vp, vp, i64, u32, C.POINTER(TbnOutputs), vp, vp, sz, vp]
+        L.tbn_forward_host.restype = i32
+        L.tbn_forward_host.argtypes = [vp, vp, i64, u32, C.POINTER(TbnOutputs)]
+        L.tbn_forward_host_f64.restype = i32
+        L.tbn_forward_host_f64.argtypes = [vp, vp, i64, u32, C.POINTER(TbnOutputs)]
+        L.tbn_sparsemax.restype = i32
+        L.tbn_sparsemax.argtypes = [vp, i64, i32, vp, vp]
+        L.tbn_sparsemax_host_f64.restype = i32
+        L.tbn_sparsemax_host_f64.argtypes = [vp, i64, i32, vp]
+        L.tbn_crc32c.restype = u32
+        L.tbn_crc32c.argtypes = [C.c_char_p, sz, u32]
+        if L.tbn_abi_version() != 1:
+            raise DeviceError("libtabnet_b200.so ABI version mismatch")
+        _lib = L
+        return _lib
+
+
+def last_error() -> str:
+    return lib().tbn_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str = "") -> None:
+    """Map tbn_status onto the reference's exception classes (errors.py:8-13)."""
+    if status == TBN_OK:
+        return
+    msg = last_error() or what
+    if status == TBN_ERR_INVALID_INPUT:
+        raise InvalidInputError(msg)
+    if status == TBN_ERR_CONFIG:
+        raise ConfigurationError(msg)
+    if status in (TBN_ERR_CUDA, TBN_ERR_UNSUPPORTED):
+        raise DeviceError(msg)
+    raise TabserveError(f"status {status}: {msg}")
+
+
+def device_count() -> int:
+    return int(lib().tbn_device_count())
+
+
+def crc32c(data: bytes, crc: int = 0) -> int:
+    return int(lib().tbn_crc32c(data, len(data), crc))
+
+
+def ptr(a: np.ndarray | None) -> int | None:
+    return None if a is None else a.ctypes.data
+
+
+def env_device() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0")) if "TBN_DEVICE" not in os.environ \
+        else int(os.environ["TBN_DEVICE"])

@@ -1,0 +1,536 @@
+// capi.cu — the C ABI of libtabnet_b200.so (include/tabnet_b200.h).
+//
+// Owns: parameter validation mirroring ModelConfig/TabNetModel (config.py:29-41,
+// network.py:110-114, network.py:207-211), the weight packer K0 (f64 params
+// dict -> device layouts), the dispatch to the fused forward kernels, and the
+// host-buffer path (pinned staging on a per-thread stream) that the
+// reference-facing Python apply() and bench.py's e2e leg use.
+#include "tabnet_b200.h"
+#include "tbn_internal.h"
+#include "tbn_tc.h"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+tbn_status fail(tbn_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+tbn_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(TBN_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TBN_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct tbn_model {
+  tbn_config cfg{};
+  int precision = TBN_PREC_TF32X3;
+  int device = 0;
+  int num_sms = 148;
+  float* d_simt = nullptr;     // fp32 copies for the CUDA-core kernel
+  tbn::SimtParams simt{};
+  tbn::TcModel tc{};           // packed tcgen05 operands (kernel_tc.cu)
+};
+
+extern "C" {
+
+int32_t tbn_abi_version(void) { return TBN_ABI_VERSION; }
+const char* tbn_last_error(void) { return g_last_error.c_str(); }
+
+int32_t tbn_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,
+                            const double* const* values, const int64_t* sizes,
+                            int32_t n_params, const double* norm_mean,
+                            const double* norm_var, int32_t precision,
+                            int32_t device, tbn_model** out) {
+  if (!cfg || !out || (!names && n_params > 0) || !norm_mean || !norm_var)
+    return fail(TBN_ERR_CONFIG, "null argument");
+  *out = nullptr;
+  const tbn_config c = *cfg;
+  // ModelConfig.__post_init__ (config.py:29-41)
+  if (c.feature_count < 1) return fail(TBN_ERR_CONFIG, "feature_count must be >= 1");
+  if (c.n_classes < 2) return fail(TBN_ERR_CONFIG, "n_classes must be >= 2");
+  if (c.n_d < 1 || c.n_a < 1) return fail(TBN_ERR_CONFIG, "n_d and n_a must be >= 1");
+  if (c.n_steps < 1) return fail(TBN_ERR_CONFIG, "n_steps must be >= 1");
+  if (!(c.gamma >= 1.0)) return fail(TBN_ERR_CONFIG, "gamma must be >= 1");
+  if (precision < TBN_PREC_TF32X3 || precision > TBN_PREC_FP32)
+    return fail(TBN_ERR_CONFIG, "unknown precision");
+  const int F = c.feature_count, ND = c.n_d, NA = c.n_a, S = c.n_steps, C = c.n_classes;
+  const int H = ND + NA, N2 = 2 * H;
+  // TabNetModel.__post_init__ (network.py:113-114)
+  for (int f = 0; f < F; ++f)
+    if (!(norm_var[f] > 0.0)) return fail(TBN_ERR_CONFIG, "normalization variances must be > 0");
+
+  // params dict by name (init_parameters, network.py:81-96)
+  std::map<std::string, std::pair<const double*, int64_t>> pm;
+  for (int i = 0; i < n_params; ++i) {
+    if (!names[i] || !values[i]) return fail(TBN_ERR_CONFIG, "null param entry");
+    pm[names[i]] = {values[i], sizes[i]};
+  }
+  auto need = [&](const std::string& k, int64_t n, const double** p) -> tbn_status {
+    auto it = pm.find(k);
+    if (it == pm.end()) return fail(TBN_ERR_CONFIG, "missing parameter " + k);
+    if (it->second.second != n)
+      return fail(TBN_ERR_CONFIG, "parameter " + k + " has " + std::to_string(it->second.second) +
+                                      " elements, expected " + std::to_string(n));
+    *p = it->second.first;
+    return TBN_OK;
+  };
+  tbn::HostParams hp;
+  hp.F = F; hp.ND = ND; hp.NA = NA; hp.S = S; hp.C = C; hp.gamma = c.gamma;
+  tbn_status st;
+  if ((st = need("shared1_W", (int64_t)F * N2, &hp.sh1_W)) != TBN_OK) return st;
+  if ((st = need("shared1_b", N2, &hp.sh1_b)) != TBN_OK) return st;
+  if ((st = need("shared2_W", (int64_t)H * N2, &hp.sh2_W)) != TBN_OK) return st;
+  if ((st = need("shared2_b", N2, &hp.sh2_b)) != TBN_OK) return st;
+  if ((st = need("head_W", (int64_t)ND * C, &hp.head_W)) != TBN_OK) return st;
+  if ((st = need("head_b", C, &hp.head_b)) != TBN_OK) return st;
+  hp.fc1_W.resize(S + 1); hp.fc1_b.resize(S + 1); hp.fc2_W.resize(S + 1); hp.fc2_b.resize(S + 1);
+  hp.att_W.resize(S + 1, nullptr); hp.att_b.resize(S + 1, nullptr);
+  for (int s = 0; s <= S; ++s) {
+    std::string p = "step" + std::to_string(s) + "_";
+    if ((st = need(p + "fc1_W", (int64_t)H * N2, &hp.fc1_W[s])) != TBN_OK) return st;
+    if ((st = need(p + "fc1_b", N2, &hp.fc1_b[s])) != TBN_OK) return st;
+    if ((st = need(p + "fc2_W", (int64_t)H * N2, &hp.fc2_W[s])) != TBN_OK) return st;
+    if ((st = need(p + "fc2_b", N2, &hp.fc2_b[s])) != TBN_OK) return st;
+    if (s >= 1) {
+      if ((st = need(p + "att_W", (int64_t)NA * F, &hp.att_W[s])) != TBN_OK) return st;
+      if ((st = need(p + "att_b", F, &hp.att_b[s])) != TBN_OK) return st;
+    }
+  }
+  hp.norm_mean = norm_mean;
+  hp.norm_var = norm_var;
+
+  int ndev = tbn_device_count();
+  if (ndev <= 0) return fail(TBN_ERR_CUDA, "no CUDA device available (this engine has no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(TBN_ERR_CONFIG, "device index out of range");
+  if (precision != TBN_PREC_FP32 && !tbn::tc_supported(hp, precision))
+    return fail(TBN_ERR_UNSUPPORTED, "no tcgen05 kernel instance for this model shape/precision");
+
+  DeviceGuard guard(device);
+  tbn_model* m = new tbn_model();
+  m->cfg = c;
+  m->precision = precision;
+  m->device = device;
+  cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
+
+  // ---- fp32 copies (scale/shift + all params) for the CUDA-core kernel ----
+  std::vector<float> buf;
+  auto put = [&](const double* src, size_t n) -> size_t {
+    size_t off = align_up(buf.size(), 32);
+    buf.resize(off + n, 0.0f);
+    for (size_t i = 0; i < n; ++i) buf[off + i] = (float)src[i];
+    return off;
+  };
+  std::vector<double> scale(F), shift(F);
+  for (int f = 0; f < F; ++f) {
+    scale[f] = 1.0 / std::sqrt(norm_var[f] + 1e-8);   // network.py:120
+    shift[f] = norm_mean[f];
+  }
+  size_t o_scale = put(scale.data(), F), o_shift = put(shift.data(), F);
+  size_t o_sh1W = put(hp.sh1_W, (size_t)F * N2), o_sh1b = put(hp.sh1_b, N2);
+  size_t o_sh2W = put(hp.sh2_W, (size_t)H * N2), o_sh2b = put(hp.sh2_b, N2);
+  size_t o_fc1W = 0, o_fc1b = 0, o_fc2W = 0, o_fc2b = 0, o_attW = 0, o_attb = 0;
+  size_t o_hW = put(hp.head_W, (size_t)ND * C), o_hb = put(hp.head_b, C);
+  // Per-step tensors are stacked densely, (s * H * N2) indexing in the kernel.
+  {
+    std::vector<float> dense;
+    auto dput = [&](const std::vector<const double*>& v, int s0, int s1, size_t n) -> size_t {
+      size_t off = align_up(dense.size(), 32);
+      dense.resize(off + n * (s1 - s0 + 1), 0.0f);
+      for (int s = s0; s <= s1; ++s)
+        for (size_t i = 0; i < n; ++i) dense[off + (size_t)(s - s0) * n + i] = (float)v[s][i];
+      return off;
+    };
+    size_t base = align_up(buf.size(), 32);
+    o_fc1W = base + dput(hp.fc1_W, 0, S, (size_t)H * N2);
+    o_fc1b = base + dput(hp.fc1_b, 0, S, N2);
+    o_fc2W = base + dput(hp.fc2_W, 0, S, (size_t)H * N2);
+    o_fc2b = base + dput(hp.fc2_b, 0, S, N2);
+    o_attW = base + dput(hp.att_W, 1, S, (size_t)NA * F);
+    o_attb = base + dput(hp.att_b, 1, S, F);
+    buf.resize(base + dense.size());
+    std::memcpy(buf.data() + base, dense.data(), dense.size() * sizeof(float));
+  }
+  cudaError_t e = cudaMalloc(&m->d_simt, buf.size() * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpy(m->d_simt, buf.data(), buf.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(m->d_simt);
+    delete m;
+    return cuda_fail(e, "uploading model");
+  }
+  float* d = m->d_simt;
+  tbn::SimtParams& sp = m->simt;
+  sp.F = F; sp.ND = ND; sp.NA = NA; sp.S = S; sp.C = C; sp.H = H; sp.gamma = (float)c.gamma;
+  sp.scale = d + o_scale; sp.shift = d + o_shift;
+  sp.sh1_W = d + o_sh1W; sp.sh1_b = d + o_sh1b; sp.sh2_W = d + o_sh2W; sp.sh2_b = d + o_sh2b;
+  sp.fc1_W = d + o_fc1W; sp.fc1_b = d + o_fc1b; sp.fc2_W = d + o_fc2W; sp.fc2_b = d + o_fc2b;
+  sp.att_W = d + o_attW; sp.att_b = d + o_attb; sp.head_W = d + o_hW; sp.head_b = d + o_hb;
+
+  // ---- tcgen05 operand packing (K0) ----
+  if (precision != TBN_PREC_FP32) {
+    std::string err;
+    if (!tbn::tc_pack(hp, precision, &m->tc, &err)) {
+      cudaFree(m->d_simt);
+      delete m;
+      return fail(TBN_ERR_CUDA, "tcgen05 weight packing failed: " + err);
+    }
+  }
+  *out = m;
+  return TBN_OK;
+}
+
+void tbn_model_destroy(tbn_model* m) {
+  if (!m) return;
+  DeviceGuard guard(m->device);
+  cudaFree(m->d_simt);
+  tbn::tc_free(&m->tc);
+  delete m;
+}
+
+tbn_status tbn_model_info(const tbn_model* m, tbn_config* cfg, int32_t* precision, int32_t* device) {
+  if (!m) return fail(TBN_ERR_CONFIG, "null model");
+  if (cfg) *cfg = m->cfg;
+  if (precision) *precision = m->precision;
+  if (device) *device = m->device;
+  return TBN_OK;
+}
+
+size_t tbn_workspace_bytes(const tbn_model* m, int64_t rows, uint32_t flags) {
+  (void)rows;
+  size_t b = 256;
+  if (m && (flags & TBN_FLAG_BATCH_STATS)) b += align_up(2 * (size_t)m->cfg.feature_count * sizeof(float), 256);
+  return b;
+}
+
+tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_t flags,
+                       const tbn_outputs* out, int32_t* err_flag, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (!m) return fail(TBN_ERR_CONFIG, "null model");
+  if (rows < 0) return fail(TBN_ERR_INVALID_INPUT, "rows must be >= 0");
+  if (rows == 0) return TBN_OK;
+  if (!x) return fail(TBN_ERR_INVALID_INPUT, "null input");
+  if ((flags & TBN_FLAG_NORMALIZED) && (flags & TBN_FLAG_BATCH_STATS)) flags &= ~TBN_FLAG_BATCH_STATS;
+  if (workspace_bytes < tbn_workspace_bytes(m, rows, flags) || !workspace)
+    return fail(TBN_ERR_CONFIG, "workspace too small");
+  DeviceGuard guard(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  tbn::ForwardArgs a{};
+  a.x = x;
+  a.rows = rows;
+  a.normalized = (flags & TBN_FLAG_NORMALIZED) ? 1 : 0;
+  if (out) {
+    a.logits = out->logits; a.probs = out->probabilities; a.masks = out->masks;
+    a.importance = out->importance; a.pred = out->predicted_class;
+  }
+  a.err_flag = err_flag;
+  if (flags & TBN_FLAG_BATCH_STATS) {
+    float* ss = (float*)((char*)workspace + 256);
+    a.scale = ss;
+    a.shift = ss + m->cfg.feature_count;
+    TBN_CUDA(tbn::launch_batch_stats(x, rows, m->cfg.feature_count, ss, ss + m->cfg.feature_count, s));
+  }
+  cudaError_t e;
+  if (m->precision == TBN_PREC_FP32)
+    e = tbn::launch_simt(m->simt, a, m->num_sms, s);
+  else
+    e = tbn::launch_tc(m->tc, a, m->num_sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
+  return TBN_OK;
+}
+
+}  // extern "C"
+
+// ------------------------- host-buffer path -------------------------------
+// Reference-facing synchronous call with HOST buffers.  The batch is cut into
+// row chunks that flow through kNumStreams streams, so chunk i's H2D, chunk
+// i-1's kernel and chunk i-2's D2H overlap (PCIe is full duplex).  Page-locked
+// caller buffers (cudaHostAlloc / torch pin_memory) are DMA'd directly; other
+// buffers (and the float64 numpy path) are staged through per-stream pinned
+// memory with the f64<->f32 conversion fused into the staging copy.
+// Per-row results are bitwise independent of the chunking (invariance contract).
+namespace {
+
+constexpr int kNumStreams = 3;
+constexpr int64_t kMinChunk = 8192;
+
+struct StreamCtx {
+  cudaStream_t stream = nullptr;
+  void* pin = nullptr;  size_t pin_bytes = 0;
+  void* dev = nullptr;  size_t dev_bytes = 0;
+  int64_t pending_r0 = -1, pending_rows = 0;   // chunk whose staged outputs await copy-out
+};
+
+struct HostCtx {
+  StreamCtx s[kNumStreams];
+};
+
+HostCtx* host_ctx(int device) {
+  // Per-thread, per-device: apply() is reentrant and 32
+  // concurrent callers (invariance.py:40-41) never share buffers or streams.
+  // Intentionally leaked at thread exit (CUDA may already be torn down).
+  thread_local std::map<int, HostCtx*> ctxs;
+  auto it = ctxs.find(device);
+  if (it != ctxs.end()) return it->second;
+  HostCtx* c = new HostCtx();
+  for (auto& sc : c->s)
+    if (cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  ctxs[device] = c;
+  return c;
+}
+
+cudaError_t ensure(StreamCtx* c, size_t pin_bytes, size_t dev_bytes) {
+  if (c->pin_bytes < pin_bytes) {
+    if (c->pin) cudaFreeHost(c->pin);
+    c->pin = nullptr; c->pin_bytes = 0;
+    cudaError_t e = cudaMallocHost(&c->pin, pin_bytes);
+    if (e != cudaSuccess) return e;
+    c->pin_bytes = pin_bytes;
+  }
+  if (c->dev_bytes < dev_bytes) {
+    if (c->dev) cudaFree(c->dev);
+    c->dev = nullptr; c->dev_bytes = 0;
+    cudaError_t e = cudaMalloc(&c->dev, dev_bytes);
+    if (e != cudaSuccess) return e;
+    c->dev_bytes = dev_bytes;
+  }
+  return cudaSuccess;
+}
+
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+struct Layout {
+  size_t x, logits, probs, masks, imp, pred, err, ws, total;
+};
+
+Layout layout_for(const tbn_model* m, int64_t rows, uint32_t flags) {
+  const size_t F = m->cfg.feature_count, C = m->cfg.n_classes, S = m->cfg.n_steps, R = rows;
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  L.x = take(R * F * 4);
+  L.logits = take(R * C * 4);
+  L.probs = take(R * C * 4);
+  L.masks = take(S * R * F * 4);
+  L.imp = take(R * F * 4);
+  L.pred = take(R * 4);
+  L.err = take(4);
+  L.ws = take(tbn_workspace_bytes(m, rows, flags));
+  L.total = o;
+  return L;
+}
+
+template <typename D, typename S_>
+void convert(D* dst, const S_* src, size_t n) {
+  for (size_t i = 0; i < n; ++i) dst[i] = (D)src[i];
+}
+
+template <typename T, typename OutT>
+tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint32_t flags,
+                             const OutT* out) {
+  if (!m) return fail(TBN_ERR_CONFIG, "null model");
+  if (rows < 0) return fail(TBN_ERR_INVALID_INPUT, "rows must be >= 0");
+  if (rows == 0) return TBN_OK;
+  if (!x) return fail(TBN_ERR_INVALID_INPUT, "null input");
+  DeviceGuard guard(m->device);
+  HostCtx* hc = host_ctx(m->device);
+  if (!hc) return fail(TBN_ERR_CUDA, "cannot create streams");
+  const size_t F = m->cfg.feature_count, C = m->cfg.n_classes, S = m->cfg.n_steps;
+  OutT o{};
+  if (out) o = *out;
+  constexpr bool kF32 = sizeof(T) == 4;
+  const bool direct = kF32 && is_pinned(x) && is_pinned(o.logits) && is_pinned(o.probabilities) &&
+                      is_pinned(o.masks) && is_pinned(o.importance) && is_pinned(o.predicted_class);
+  // Batch statistics (negative control) need the whole batch in one call.
+  int64_t chunk = rows;
+  if (!(flags & TBN_FLAG_BATCH_STATS) && rows > 2 * kMinChunk) {
+    chunk = (rows + kNumStreams - 1) / kNumStreams;
+    chunk = ((chunk + 127) / 128) * 128;
+    if (chunk < kMinChunk) chunk = kMinChunk;
+  }
+  const Layout L = layout_for(m, chunk, flags);
+  for (auto& sc : hc->s) {
+    TBN_CUDA(ensure(&sc, direct ? 256 : L.total, L.total));
+    sc.pending_r0 = -1;
+  }
+  int32_t err_any = 0;
+  const size_t err_off = direct ? 0 : L.err;   // pinned landing slot of the chunk's error flag
+  // copy a finished chunk's staged outputs into the caller's arrays
+  auto drain = [&](StreamCtx& sc) -> tbn_status {
+    if (sc.pending_r0 < 0) return TBN_OK;
+    TBN_CUDA(cudaStreamSynchronize(sc.stream));
+    char* P = (char*)sc.pin;
+    const size_t r0 = sc.pending_r0, n = sc.pending_rows;
+    err_any |= *(int32_t*)(P + err_off);
+    if (!direct) {
+      if (o.logits) convert(o.logits + r0 * C, (const float*)(P + L.logits), n * C);
+      if (o.probabilities) convert(o.probabilities + r0 * C, (const float*)(P + L.probs), n * C);
+      if (o.masks)
+        for (size_t s = 0; s < S; ++s)
+          convert(o.masks + (s * rows + r0) * F, (const float*)(P + L.masks) + s * n * F, n * F);
+      if (o.importance) convert(o.importance + r0 * F, (const float*)(P + L.imp), n * F);
+      if (o.predicted_class) std::memcpy(o.predicted_class + r0, P + L.pred, n * 4);
+    }
+    sc.pending_r0 = -1;
+    return TBN_OK;
+  };
+  int ci = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk, ++ci) {
+    StreamCtx& sc = hc->s[ci % kNumStreams];
+    tbn_status st = drain(sc);
+    if (st != TBN_OK) return st;
+    const int64_t n = (rows - r0 < chunk) ? rows - r0 : chunk;
+    char* P = (char*)sc.pin;
+    char* D = (char*)sc.dev;
+    cudaStream_t cs = sc.stream;
+    TBN_CUDA(cudaMemsetAsync(D + L.err, 0, 4, cs));
+    if (direct) {
+      TBN_CUDA(cudaMemcpyAsync(D + L.x, (const float*)x + r0 * F, n * F * 4, cudaMemcpyHostToDevice, cs));
+    } else {
+      convert((float*)(P + L.x), x + r0 * F, n * F);
+      TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, n * F * 4, cudaMemcpyHostToDevice, cs));
+    }
+    tbn_outputs dout{};
+    dout.logits = o.logits ? (float*)(D + L.logits) : nullptr;
+    dout.probabilities = o.probabilities ? (float*)(D + L.probs) : nullptr;
+    dout.masks = o.masks ? (float*)(D + L.masks) : nullptr;
+    dout.importance = o.importance ? (float*)(D + L.imp) : nullptr;
+    dout.predicted_class = o.predicted_class ? (int32_t*)(D + L.pred) : nullptr;
+    st = tbn_forward(m, (const float*)(D + L.x), n, flags, &dout, (int32_t*)(D + L.err),
+                     D + L.ws, L.total - L.ws, cs);
+    if (st != TBN_OK) return st;
+    if (direct) {
+      float* fo;
+      if ((fo = (float*)(void*)o.logits)) TBN_CUDA(cudaMemcpyAsync(fo + r0 * C, dout.logits, n * C * 4, cudaMemcpyDeviceToHost, cs));
+      if ((fo = (float*)(void*)o.probabilities)) TBN_CUDA(cudaMemcpyAsync(fo + r0 * C, dout.probabilities, n * C * 4, cudaMemcpyDeviceToHost, cs));
+      if ((fo = (float*)(void*)o.masks))
+        TBN_CUDA(cudaMemcpy2DAsync(fo + r0 * F, rows * F * 4, dout.masks, n * F * 4, n * F * 4, S,
+                                   cudaMemcpyDeviceToHost, cs));
+      if ((fo = (float*)(void*)o.importance)) TBN_CUDA(cudaMemcpyAsync(fo + r0 * F, dout.importance, n * F * 4, cudaMemcpyDeviceToHost, cs));
+      if (o.predicted_class) TBN_CUDA(cudaMemcpyAsync(o.predicted_class + r0, dout.predicted_class, n * 4, cudaMemcpyDeviceToHost, cs));
+      TBN_CUDA(cudaMemcpyAsync(P + err_off, D + L.err, 4, cudaMemcpyDeviceToHost, cs));
+    } else {
+      if (dout.logits) TBN_CUDA(cudaMemcpyAsync(P + L.logits, dout.logits, n * C * 4, cudaMemcpyDeviceToHost, cs));
+      if (dout.probabilities) TBN_CUDA(cudaMemcpyAsync(P + L.probs, dout.probabilities, n * C * 4, cudaMemcpyDeviceToHost, cs));
+      if (dout.masks) TBN_CUDA(cudaMemcpyAsync(P + L.masks, dout.masks, S * n * F * 4, cudaMemcpyDeviceToHost, cs));
+      if (dout.importance) TBN_CUDA(cudaMemcpyAsync(P + L.imp, dout.importance, n * F * 4, cudaMemcpyDeviceToHost, cs));
+      if (dout.predicted_class) TBN_CUDA(cudaMemcpyAsync(P + L.pred, dout.predicted_class, n * 4, cudaMemcpyDeviceToHost, cs));
+      TBN_CUDA(cudaMemcpyAsync(P + L.err, D + L.err, 4, cudaMemcpyDeviceToHost, cs));
+    }
+    sc.pending_r0 = r0;
+    sc.pending_rows = n;
+  }
+  for (auto& sc : hc->s) {
+    tbn_status st = drain(sc);
+    if (st != TBN_OK) return st;
+  }
+  if (err_any) return fail(TBN_ERR_INVALID_INPUT, "features must be finite");
+  return TBN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tbn_status tbn_forward_host(const tbn_model* m, const float* x, int64_t rows, uint32_t flags,
+                            const tbn_outputs* out) {
+  return forward_host_impl(m, x, rows, flags, out);
+}
+
+tbn_status tbn_forward_host_f64(const tbn_model* m, const double* x, int64_t rows, uint32_t flags,
+                                const tbn_outputs_f64* out) {
+  return forward_host_impl(m, x, rows, flags, out);
+}
+
+tbn_status tbn_sparsemax(const float* z, int64_t rows, int32_t n, float* out, void* stream) {
+  if (rows < 0 || n < 1) return fail(TBN_ERR_INVALID_INPUT, "sparsemax input must have length >= 1");
+  if (n > 512) return fail(TBN_ERR_UNSUPPORTED, "sparsemax width > 512");
+  if (rows == 0) return TBN_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = tbn::launch_sparsemax(z, rows, n, out, nullptr, sms, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sparsemax launch");
+  return TBN_OK;
+}
+
+tbn_status tbn_sparsemax_host_f64(const double* z, int64_t rows, int32_t n, double* out) {
+  if (rows < 1 || n < 1) return fail(TBN_ERR_INVALID_INPUT, "sparsemax input must have length >= 1");
+  if (n > 512) return fail(TBN_ERR_UNSUPPORTED, "sparsemax width > 512");
+  if (tbn_device_count() <= 0) return fail(TBN_ERR_CUDA, "no CUDA device available");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  HostCtx* hc = host_ctx(dev);
+  if (!hc) return fail(TBN_ERR_CUDA, "cannot create stream");
+  StreamCtx* c = &hc->s[0];
+  const size_t bytes = (size_t)rows * n * 4;
+  const size_t total = align_up(bytes, 256) * 2 + 256;
+  TBN_CUDA(ensure(c, total, total));
+  float* pz = (float*)c->pin;
+  for (size_t i = 0; i < (size_t)rows * n; ++i) pz[i] = (float)z[i];
+  char* D = (char*)c->dev;
+  float* dz = (float*)D;
+  float* dout = (float*)(D + align_up(bytes, 256));
+  int32_t* derr = (int32_t*)(D + 2 * align_up(bytes, 256));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  TBN_CUDA(cudaMemsetAsync(derr, 0, 4, c->stream));
+  TBN_CUDA(cudaMemcpyAsync(dz, pz, bytes, cudaMemcpyHostToDevice, c->stream));
+  TBN_CUDA(tbn::launch_sparsemax(dz, rows, n, dout, derr, sms, c->stream));
+  float* po = (float*)((char*)c->pin + align_up(bytes, 256));
+  int32_t* perr = (int32_t*)((char*)c->pin + 2 * align_up(bytes, 256));
+  TBN_CUDA(cudaMemcpyAsync(po, dout, bytes, cudaMemcpyDeviceToHost, c->stream));
+  TBN_CUDA(cudaMemcpyAsync(perr, derr, 4, cudaMemcpyDeviceToHost, c->stream));
+  TBN_CUDA(cudaStreamSynchronize(c->stream));
+  if (*perr) return fail(TBN_ERR_INVALID_INPUT, "sparsemax input must be finite");
+  for (size_t i = 0; i < (size_t)rows * n; ++i) out[i] = po[i];
+  return TBN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+// kernel_simt.cu — TBN_PREC_FP32: the whole TabNet forward (network.py:195-267)
+// as ONE kernel on CUDA cores, one warp per row, fp32 FFMA.  This is the
+// no-tensor-core precision reference of the engine (and the first correct
+// path); the production path is kernel_tc.cu (tcgen05).
+//
+// Per-row results depend only on the row (fixed per-lane k-ascending FFMA
+// chains, fixed butterfly reductions), never on batch size, warp or block
+// position: the batch-invariance contract of network.py:11-14.
+#include "tbn_internal.h"
+#include "tbn_device.cuh"
+
+namespace tbn {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kMaxF = 512;
+constexpr int kMaxN = 256;            // 2h
+constexpr int kFPerLane = kMaxF / 32; // 16
+
+// out[n] = b[n] + sum_k in[k] * W[k*N + n]   (x @ W + b, network.py:127 etc.)
+__device__ __forceinline__ void warp_gemv(const float* __restrict__ in, int K,
+                                          const float* __restrict__ W,
+                                          const float* __restrict__ b, int N,
+                                          float* __restrict__ out, int lane) {
+  for (int n0 = 0; n0 < N; n0 += 128) {
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k = 0; k < K; ++k) {
+      float a = in[k];
+      const float* wr = W + (size_t)k * N;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int n = n0 + lane + 32 * j;
+        if (n < N) acc[j] = fmaf(a, __ldg(wr + n), acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + lane + 32 * j;
+      if (n < N) out[n] = acc[j] + __ldg(b + n);
+    }
+  }
+}
+
+// g = GLU(u) [+ residual]:  u[:, :h] * sigmoid(u[:, h:])   (network.py:58-61, 131-137)
+__device__ __forceinline__ void warp_glu(const float* __restrict__ u, float* g, int H,
+                                         bool residual, int lane) {
+  for (int j = lane; j < H; j += 32) {
+    float v = u[j] * sigmoid_accurate(u[H + j]);
+    g[j] = residual ? (v + g[j]) * kResidualScale : v;
+  }
+}
+
+// Feature transformer (network.py:124-141): shared1 -> shared2 -> fc1_s -> fc2_s.
+__device__ __forceinline__ void warp_transform(const SimtParams& p, const float* xin,
+                                               float* u, float* g, int step, int lane) {
+  const int H = p.H, N = 2 * p.H;
+  warp_gemv(xin, p.F, p.sh1_W, p.sh1_b, N, u, lane);
+  __syncwarp();
+  warp_glu(u, g, H, false, lane);
+  __syncwarp();
+  warp_gemv(g, H, p.sh2_W, p.sh2_b, N, u, lane);
+  __syncwarp();
+  warp_glu(u, g, H, true, lane);
+  __syncwarp();
+  warp_gemv(g, H, p.fc1_W + (size_t)step * H * N, p.fc1_b + (size_t)step * N, N, u, lane);
+  __syncwarp();
+  warp_glu(u, g, H, true, lane);
+  __syncwarp();
+  warp_gemv(g, H, p.fc2_W + (size_t)step * H * N, p.fc2_b + (size_t)step * N, N, u, lane);
+  __syncwarp();
+  warp_glu(u, g, H, true, lane);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+tabnet_forward_simt(SimtParams p, ForwardArgs a) {
+  extern __shared__ float smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int F = p.F, H = p.H, ND = p.ND, S = p.S, C = p.C;
+  const int per_warp = 5 * F + 3 * H + ND + F;   // xn, prior, agg, m, xm | u(2H), g(H) | dsum | msum
+  float* base = smem + (size_t)warp * per_warp;
+  float* xn = base;
+  float* prior = xn + F;
+  float* agg = prior + F;
+  float* m = agg + F;
+  float* xm = m + F;
+  float* u = xm + F;
+  float* g = u + 2 * H;
+  float* dsum = g + H;
+  float* msum = dsum + ND;
+  const float* scale = a.scale ? a.scale : p.scale;
+  const float* shift = a.shift ? a.shift : p.shift;
+
+  for (int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + warp; row < a.rows;
+       row += (int64_t)gridDim.x * kWarpsPerBlock) {
+    // -- load + validate + normalize (network.py:207-220) --
+    int bad = 0;
+    for (int f = lane; f < F; f += 32) {
+      float xv = a.x[row * F + f];
+      bad |= !isfinite(xv);
+      xn[f] = a.normalized ? xv : (xv - shift[f]) * scale[f];
+      prior[f] = 1.0f;
+      agg[f] = 0.0f;
+      msum[f] = 0.0f;
+    }
+    if (__any_sync(kFull, bad) && lane == 0 && a.err_flag) atomicOr(a.err_flag, 1);
+    for (int j = lane; j < ND; j += 32) dsum[j] = 0.0f;
+    __syncwarp();
+    // -- step 0 transformer; a = f0[:, n_d:] (network.py:226-227) --
+    warp_transform(p, xn, u, g, 0, lane);
+    for (int s = 1; s <= S; ++s) {
+      // att = a @ W_att + b; z = prior * att (network.py:233-235)
+      const float* Wa = p.att_W + (size_t)(s - 1) * p.NA * F;
+      const float* ba = p.att_b + (size_t)(s - 1) * F;
+      float zs[kFPerLane];
+      float zmax = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kFPerLane; ++i) {
+        int f = lane + 32 * i;
+        float z = -INFINITY;
+        if (f < F) {
+          float acc = 0.0f;
+          for (int k = 0; k < p.NA; ++k) acc = fmaf(g[ND + k], __ldg(Wa + (size_t)k * F + f), acc);
+          z = prior[f] * (acc + __ldg(ba + f));
+        }
+        zs[i] = z;
+        zmax = fmaxf(zmax, z);
+      }
+      zmax = warp_max(zmax);
+#pragma unroll
+      for (int i = 0; i < kFPerLane; ++i) zs[i] -= zmax;   // sparsemax.py:32
+      const float tau = warp_sparsemax_tau(zs, F, lane);
+      float* mask_out = a.masks ? a.masks + ((size_t)(s - 1) * a.rows + row) * F : nullptr;
+#pragma unroll
+      for (int i = 0; i < kFPerLane; ++i) {
+        int f = lane + 32 * i;
+        if (f < F) {
+          float mv = fmaxf(zs[i] - tau, 0.0f);             // sparsemax.py:40
+          m[f] = mv;
+          prior[f] = prior[f] * (p.gamma - mv);            // network.py:237
+          xm[f] = mv * xn[f];                              // network.py:238
+          if (mask_out) mask_out[f] = mv;                  // network.py:246
+          msum[f] += mv;
+        }
+      }
+      __syncwarp();
+      warp_transform(p, xm, u, g, s, lane);
+      // d = relu(f[:, :n_d]); d_sum += d; eta = sum(d); agg += eta * m (network.py:241-245)
+      float eta = 0.0f;
+      for (int j = lane; j < ND; j += 32) {
+        float d = fmaxf(g[j], 0.0f);
+        dsum[j] += d;
+        eta += d;
+      }
+      eta = warp_sum(eta);
+      for (int f = lane; f < F; f += 32) agg[f] = fmaf(eta, m[f], agg[f]);
+      __syncwarp();
+    }
+    // -- head + softmax (network.py:253-256) --
+    float logit = -INFINITY;
+    if (lane < C) {
+      float acc = 0.0f;
+      for (int k = 0; k < ND; ++k) acc = fmaf(dsum[k], __ldg(p.head_W + (size_t)k * C + lane), acc);
+      logit = acc + __ldg(p.head_b + lane);
+    }
+    float lmax = warp_max(logit);
+    float e = (lane < C) ? expf(logit - lmax) : 0.0f;
+    float esum = warp_sum(e);
+    float prob = e / esum;
+    if (lane < C) {
+      if (a.logits) a.logits[row * C + lane] = logit;
+      if (a.probs) a.probs[row * C + lane] = prob;
+    }
+    // argmax, lowest index on ties
+    float bv = (lane < C) ? prob : -INFINITY;
+    int bi = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(kFull, bv, o);
+      int oi = __shfl_xor_sync(kFull, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0 && a.pred) a.pred[row] = bi;
+    // -- importance (network.py:258-261) --
+    float tot = 0.0f;
+    for (int f = lane; f < F; f += 32) tot += agg[f];
+    tot = warp_sum(tot);
+    if (a.importance) {
+      for (int f = lane; f < F; f += 32)
+        a.importance[row * F + f] = (tot > 0.0f) ? agg[f] / tot : msum[f] / (float)S;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+size_t simt_smem_bytes(const SimtParams& p) {
+  return (size_t)kWarpsPerBlock * (5 * p.F + 3 * p.H + p.ND + p.F) * sizeof(float);
+}
+
+cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  if (p.F > kMaxF || 2 * p.H > kMaxN || p.C > 32) return cudaErrorInvalidValue;
+  size_t smem = simt_smem_bytes(p);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tabnet_forward_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  int64_t blocks_needed = (a.rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int64_t max_blocks = (int64_t)num_sms * 8;
+  int grid = (int)(blocks_needed < max_blocks ? blocks_needed : max_blocks);
+  if (grid < 1) grid = 1;
+  tabnet_forward_simt<<<grid, kWarpsPerBlock * 32, smem, stream>>>(p, a);
+  return cudaGetLastError();
+}
+
+// ---- standalone sparsemax (sparsemax.py:13-41), warp per row ----
+namespace {
+__global__ void sparsemax_rows_kernel(const float* __restrict__ z, int64_t rows, int n,
+                                      float* __restrict__ out, int32_t* err_flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    float zs[kFPerLane];
+    float zmax = -INFINITY;
+    int bad = 0;
+#pragma unroll
+    for (int i = 0; i < kFPerLane; ++i) {
+      int f = lane + 32 * i;
+      float v = (f < n) ? z[r * n + f] : -INFINITY;
+      if (f < n) bad |= !isfinite(v);
+      zs[i] = v;
+      zmax = fmaxf(zmax, v);
+    }
+    if (__any_sync(kFull, bad) && lane == 0 && err_flag) atomicOr(err_flag, 1);
+    zmax = warp_max(zmax);
+#pragma unroll
+    for (int i = 0; i < kFPerLane; ++i) zs[i] -= zmax;
+    float tau = warp_sparsemax_tau(zs, n, lane);
+#pragma unroll
+    for (int i = 0; i < kFPerLane; ++i) {
+      int f = lane + 32 * i;
+      if (f < n) out[r * n + f] = fmaxf(zs[i] - tau, 0.0f);
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_sparsemax(const float* z, int64_t rows, int n, float* out, int32_t* err_flag,
+                             int num_sms, cudaStream_t stream) {
+  if (n > kMaxF) return cudaErrorInvalidValue;
+  int64_t blocks = (rows + 7) / 8;
+  int64_t cap = (int64_t)num_sms * 16;
+  int grid = (int)(blocks < cap ? blocks : cap);
+  if (grid < 1) grid = 1;
+  sparsemax_rows_kernel<<<grid, 256, 0, stream>>>(z, rows, n, out, err_flag);
+  return cudaGetLastError();
+}
+
+}  // namespace tbn

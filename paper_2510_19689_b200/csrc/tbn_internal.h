@@ -1,0 +1,44 @@
+// tbn_internal.h — internal (non-ABI) declarations of libtabnet_b200.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tbn {
+
+// Pointers into the model's device buffer, fp32 row-major copies of the
+// reference params dict (network.py:81-96), used by the CUDA-core kernel.
+struct SimtParams {
+  int F, ND, NA, S, C, H;
+  float gamma;
+  const float* scale;   // (F)  1/sqrt(var+eps)          (network.py:120)
+  const float* shift;   // (F)  mean
+  const float* sh1_W; const float* sh1_b;   // (F,2H) (2H)
+  const float* sh2_W; const float* sh2_b;   // (H,2H) (2H)
+  const float* fc1_W; const float* fc1_b;   // (S+1,H,2H) (S+1,2H)
+  const float* fc2_W; const float* fc2_b;
+  const float* att_W; const float* att_b;   // (S,NA,F) (S,F)   index s-1
+  const float* head_W; const float* head_b; // (ND,C) (C)
+};
+
+struct ForwardArgs {
+  const float* x;
+  int64_t rows;
+  int normalized;
+  const float* scale;   // per-call override (batch-stats control); null = model's
+  const float* shift;
+  float* logits;
+  float* probs;
+  float* masks;
+  float* importance;
+  int32_t* pred;
+  int32_t* err_flag;
+};
+
+size_t simt_smem_bytes(const SimtParams& p);
+cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, cudaStream_t stream);
+cudaError_t launch_sparsemax(const float* z, int64_t rows, int n, float* out, int32_t* err_flag,
+                             int num_sms, cudaStream_t stream);
+cudaError_t launch_batch_stats(const float* x, int64_t rows, int F, float* scale, float* shift,
+                               cudaStream_t stream);
+
+}  // namespace tbn

@@ -1,0 +1,37 @@
+// tbn_tc.h — the tcgen05 fused forward (kernel_tc.cu): host-side packing (K0)
+// and launch interface.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+#include "tbn_internal.h"
+
+namespace tbn {
+
+// Borrowed views of the reference params dict (float64, row-major, x @ W).
+struct HostParams {
+  int F = 0, ND = 0, NA = 0, S = 0, C = 0;
+  double gamma = 1.3;
+  const double* sh1_W = nullptr; const double* sh1_b = nullptr;
+  const double* sh2_W = nullptr; const double* sh2_b = nullptr;
+  std::vector<const double*> fc1_W, fc1_b, fc2_W, fc2_b;   // index s = 0..S
+  std::vector<const double*> att_W, att_b;                 // index s = 1..S (0 unused)
+  const double* head_W = nullptr; const double* head_b = nullptr;
+  const double* norm_mean = nullptr; const double* norm_var = nullptr;
+};
+
+struct TcModel {
+  int shape_id = -1;       // which compiled instance
+  int precision = 0;
+  void* d_buf = nullptr;   // packed operands + epilogue constants
+  size_t bytes = 0;
+  void* params = nullptr;  // host copy of the kernel's parameter block
+};
+
+bool tc_supported(const HostParams& hp, int precision);
+bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
+void tc_free(TcModel* m);
+cudaError_t launch_tc(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream);
+
+}  // namespace tbn

@@ -1,0 +1,66 @@
+"""Tie-aware parity comparator shared by the GPU tests.
+
+A row is EXEMPT when the float64 reference's own sparsemax margin at any step,
+min_i |z_i - tau| / max|z|, is below ``delta`` (the support set there is decided
+by rounding, not by the model), or — for the class check only — when its top-2
+probability gap is below ``gap``.  On every other row: identical sparsemax
+support sets at every step, identical predicted class, and values within
+``|gpu - ref| <= rtol*|ref| + atol``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class ParityReport:
+    rows: int
+    exempt_rows: list = field(default_factory=list)
+    support_mismatch_rows: list = field(default_factory=list)
+    class_mismatch_rows: list = field(default_factory=list)
+    max_err: dict = field(default_factory=dict)
+    viol: dict = field(default_factory=dict)
+
+    @property
+    def ok(self) -> bool:
+        return not self.support_mismatch_rows and not self.class_mismatch_rows and \
+            all(v == 0 for v in self.viol.values())
+
+    def summary(self) -> str:
+        return (f"rows={self.rows} exempt={len(self.exempt_rows)} "
+                f"support_mismatch={self.support_mismatch_rows[:10]} "
+                f"class_mismatch={self.class_mismatch_rows[:10]} "
+                f"max_err={ {k: float(f'{v:.3g}') for k, v in self.max_err.items()} } viol={self.viol}")
+
+
+def compare(ref: dict, got: dict, *, delta: float = 1e-4, gap: float = 1e-6,
+            rtol: float = 1e-4, atol: dict | None = None) -> ParityReport:
+    atol = {"logits": 1e-6, "probabilities": 1e-6, "masks": 1e-6, "importance": 1e-6,
+            **(atol or {})}
+    margin = ref["margin"]                   # (S, B)
+    b = margin.shape[1]
+    exempt = np.any(margin < delta, axis=0)
+    rep = ParityReport(rows=b, exempt_rows=np.nonzero(exempt)[0].tolist())
+    keep = ~exempt
+    sup_ref = ref["masks"] > 0
+    sup_got = np.asarray(got["masks"]) > 0
+    sup_bad = np.any(sup_ref != sup_got, axis=(0, 2)) & keep
+    rep.support_mismatch_rows = np.nonzero(sup_bad)[0].tolist()
+    cls_ref = np.argmax(ref["probabilities"], axis=1)
+    cls_got = np.argmax(np.asarray(got["probabilities"]), axis=1)
+    cls_keep = keep & (ref["top2_gap"] >= gap)
+    rep.class_mismatch_rows = np.nonzero((cls_ref != cls_got) & cls_keep)[0].tolist()
+    for k in ("logits", "probabilities", "importance", "masks"):
+        r = np.asarray(ref[k], dtype=np.float64)
+        g = np.asarray(got[k], dtype=np.float64)
+        if k == "masks":
+            r, g = r[:, keep], g[:, keep]
+        else:
+            r, g = r[keep], g[keep]
+        err = np.abs(g - r)
+        rep.max_err[k] = float(err.max()) if err.size else 0.0
+        rep.max_err[k + "_rel"] = float((err / np.maximum(np.abs(r), 1e-30)).max()) if err.size else 0.0
+        rep.viol[k] = int(np.count_nonzero(err > rtol * np.abs(r) + atol[k]))
+    return rep

@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path against the reference-pinned oracle/goldens.
+
+Tie-aware rule (parity.py): on every row whose reference
+sparsemax margin is >= 1e-4 at all steps, identical support sets and class and
+values within 1e-4 relative (+1e-6 absolute).  Exempt rows are counted.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from parity import compare
+import paper_2510_19689_b200 as P
+from paper_2510_19689_b200 import workloads as W
+from oracle import tabnet_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+# precisions with a compiled kernel, and the bound each is held to
+EXACT_PRECISIONS = ["fp32"]
+CASES = [f"{n}_{r}" for n in ("adult", "hr", "bls", "wide") for r in ("init", "trained")]
+_NAMES = {"adult": "adult", "hr": "hr", "bls": "bls", "wide": "wide"}
+
+
+def golden_model(case: str, precision: str) -> P.TabNetModel:
+    g = load_golden(case)
+    f, nd, na, s, c = (int(v) for v in g["shape"])
+    cfg = P.ModelConfig(feature_count=f, n_classes=c, n_d=nd, n_a=na, n_steps=s)
+    p = P.init_parameters(cfg)
+    if str(g["regime"]) == "trained":
+        for k in list(p):
+            if k.endswith("_att_W"):
+                p[k] = p[k] * 16.0
+        p["head_W"] = p["head_W"] * 8.0
+    return P.TabNetModel(config=cfg, params=p, norm_mean=g["norm_mean"], norm_var=g["norm_var"],
+                         model_version=case, precision=precision)
+
+
+def _res_dict(r):
+    return dict(logits=r.logits, probabilities=r.probabilities, masks=r.masks,
+                importance=r.importance)
+
+
+@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+@pytest.mark.parametrize("case", CASES)
+def test_parity_against_reference_goldens(case, precision):
+    g = load_golden(case)
+    m = golden_model(case, precision)
+    r = m.apply(g["x"].astype(np.float64))
+    rep = compare(g, _res_dict(r))
+    print(case, precision, rep.summary())
+    assert rep.ok, rep.summary()
+    assert len(rep.exempt_rows) <= max(2, g["x"].shape[0] // 50)
+
+
+@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+def test_full_size_hr_against_oracle(precision):
+    """HR @ 65,536 rows (BASELINE config 1) against the oracle on every row."""
+    m = W.make_model("hr", "trained", model_cls=None)
+    m = P.TabNetModel.from_reference(m, precision=precision)
+    x = W.make_inputs(W.WORKLOADS["hr"], 65536).astype(np.float64)
+    ref = O.apply_model(m, x, diagnostics=True)
+    zs, tau = ref["z_shift"], ref["tau"]
+    scale = np.maximum(np.abs(zs).max(axis=2), 1e-300)
+    ref["margin"] = np.abs(zs - tau[..., None]).min(axis=2) / scale
+    p = np.sort(ref["probabilities"], axis=1)
+    ref["top2_gap"] = p[:, -1] - p[:, -2]
+    r = m.apply(x)
+    rep = compare(ref, _res_dict(r))
+    print("hr65536", precision, rep.summary())
+    assert rep.ok, rep.summary()
+    assert len(rep.exempt_rows) < 65536 // 100
+    # size-independent properties on all rows
+    np.testing.assert_allclose(r.masks.sum(axis=2), 1.0, atol=1e-5)
+    assert np.all(r.masks >= 0)
+    np.testing.assert_allclose(r.importance.sum(axis=1), 1.0, atol=1e-5)
+    np.testing.assert_allclose(r.probabilities.sum(axis=1), 1.0, atol=1e-6)
+
+
+@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+def test_importance_fallback_rows(precision):
+    g = load_golden("adult_fallback")
+    cfg = P.ModelConfig(feature_count=14, n_classes=2, n_d=8, n_a=8, n_steps=3)
+    m = P.TabNetModel(config=cfg, params=P.init_parameters(cfg), norm_mean=g["norm_mean"],
+                      norm_var=g["norm_var"], model_version="fb", precision=precision)
+    r = m.apply(g["x"].astype(np.float64))
+    fb = g["fallback_rows"]
+    np.testing.assert_allclose(r.importance[fb], r.masks.mean(axis=0)[fb], atol=1e-6)
+    np.testing.assert_allclose(r.importance, g["importance"], atol=1e-5)
+
+
+def _explanations(model, x, batch_size, concurrency, use_batch_stats):
+    # restatement of interpret/invariance.py:24-45
+    chunks = [(i, x[i:i + batch_size]) for i in range(0, x.shape[0], batch_size)]
+    masks = np.empty((model.config.n_steps, x.shape[0], x.shape[1]))
+    imp = np.empty((x.shape[0], x.shape[1]))
+
+    def run(item):
+        start, chunk = item
+        return start, chunk.shape[0], model.apply(chunk, use_batch_stats=use_batch_stats)
+
+    if concurrency <= 1:
+        results = [run(c) for c in chunks]
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=concurrency) as pool:
+            results = list(pool.map(run, chunks))
+    for start, n, res in results:
+        masks[:, start:start + n, :] = res.masks
+        imp[start:start + n, :] = res.importance
+    return masks, imp
+
+
+def load_invariance_check(model, x, concurrency=(1, 32), batch_sizes=(1, 256), use_batch_stats=False):
+    # restatement of interpret/invariance.py:56-82
+    bm, bi = _explanations(model, x, batch_sizes[0], concurrency[0], use_batch_stats)
+    for conc in set(concurrency):
+        for bs in set(batch_sizes):
+            m, i = _explanations(model, x, bs, conc, use_batch_stats)
+            if not (np.array_equal(m, bm) and np.array_equal(i, bi)):
+                return False
+    return True
+
+
+@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+def test_load_invariance_bitwise(precision):
+    m = P.TabNetModel.from_reference(W.make_model("hr"), precision=precision)
+    x = W.make_inputs(W.WORKLOADS["hr"], 512).astype(np.float64)
+    assert load_invariance_check(m, x)
+    # negative control must be caught (invariance.py:59,67-71)
+    assert not load_invariance_check(m, x, use_batch_stats=True)
+
+
+@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+def test_nonfinite_and_width_errors(precision):
+    m = P.TabNetModel.from_reference(W.make_model("adult"), precision=precision)
+    x = np.zeros((300, 14))
+    x[217, 3] = np.nan
+    with pytest.raises(P.InvalidInputError):
+        m.apply(x)
+    x[217, 3] = np.inf
+    with pytest.raises(P.InvalidInputError):
+        m.apply(x)
+    with pytest.raises(P.InvalidInputError):
+        m.apply(np.zeros((3, 15)))
+    r = m.apply(np.zeros(14))          # 1-D input -> one row (network.py:205-206)
+    assert r.masks.shape == (3, 1, 14)
+
+
+def test_sparsemax_gpu_spec_examples():
+    g = load_golden("sparsemax_spec")
+    np.testing.assert_allclose(P.sparsemax(np.array([0.6, 0.4])), [0.6, 0.4], atol=1e-7)
+    np.testing.assert_allclose(P.sparsemax(np.array([0.37] * 3)), [1 / 3] * 3, atol=1e-7)
+    np.testing.assert_allclose(P.sparsemax(np.array([2.0, 1.0, 0.1])), [1, 0, 0], atol=1e-7)
+    np.testing.assert_allclose(P.sparsemax(g["bf_in"]), g["bf_out"], atol=2e-6)
+    np.testing.assert_allclose(P.sparsemax(g["rand64_in"]), g["rand64_out"], atol=2e-6)
+    np.testing.assert_allclose(P.sparsemax(g["rand512_in"]), g["rand512_out"], atol=5e-6)
+    with pytest.raises(P.InvalidInputError):
+        P.sparsemax(np.array([1.0, np.nan]))
+
+
+def test_attentive_step_spec():
+    # gamma = 1, mask one-hot on feature j -> new_prior[j] = 0
+    cfg = P.ModelConfig(feature_count=3, n_a=2, n_d=2, n_steps=1, gamma=1.0)
+    p = P.init_parameters(cfg)
+    p["step1_att_W"] = np.array([[10.0, 0.0, 0.0], [0.0, 0.0, 0.0]])
+    m = P.TabNetModel(config=cfg, params=p, norm_mean=np.zeros(3), norm_var=np.ones(3),
+                      model_version="t", precision="fp32")
+    mask, new_prior = m.attentive_step(np.array([1.0, 0.0]), np.ones(3), 1)
+    np.testing.assert_allclose(mask, [[1, 0, 0]], atol=1e-7)
+    np.testing.assert_allclose(new_prior, [[0, 1, 1]], atol=1e-7)
+
+
+@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+def test_forward_objects(precision):
+    m = P.TabNetModel.from_reference(W.make_model("adult"), precision=precision)
+    x = W.make_inputs(W.WORKLOADS["adult"], 33).astype(np.float64)
+    outs = m.forward(x)
+    r = m.apply(x)
+    assert len(outs) == 33
+    for i, o in enumerate(outs):
+        assert o.predicted_class == int(np.argmax(r.probabilities[i]))
+        assert np.array_equal(o.explanation.step_masks, r.masks[:, i, :])
+
+
+@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+def test_shard_and_device_path_bitwise(precision):
+    """Row shards processed as separate calls (as 1/2/4/8 GPUs would) and the
+    zero-copy torch device path are bitwise equal to one full call."""
+    import torch
+    from paper_2510_19689_b200.device import DeviceRunner
+    m = P.TabNetModel.from_reference(W.make_model("hr"), precision=precision)
+    x = W.make_inputs(W.WORKLOADS["hr"], 4099)
+    full = m.apply(x.astype(np.float64))
+    for world in (2, 4, 8):
+        bounds = np.linspace(0, x.shape[0], world + 1).astype(int)
+        parts = [m.apply(x[a:b].astype(np.float64)) for a, b in zip(bounds[:-1], bounds[1:])]
+        assert np.array_equal(np.concatenate([p.masks for p in parts], axis=1), full.masks)
+        assert np.array_equal(np.concatenate([p.importance for p in parts]), full.importance)
+    runner = DeviceRunner(m, max_rows=x.shape[0])
+    xd = torch.from_numpy(x).cuda()
+    out = runner.run(xd)
+    torch.cuda.synchronize()
+    assert np.array_equal(out["masks"].cpu().numpy().astype(np.float64), full.masks)
+    assert np.array_equal(out["probabilities"].cpu().numpy().astype(np.float64), full.probabilities)

@@ -1,16 +1,172 @@
-// kernel_tc.cu — placeholder until the tcgen05 kernel lands: no instance is
-// compiled, so model creation with a tensor-core precision reports
-// TBN_ERR_UNSUPPORTED (never a silent fallback to another kernel).
+// kernel_tc.cu — host side of K1 (tc_kernel.cuh): the weight packer K0 and the
+// per-shape kernel instances.  K0 turns the reference's float64 params dict
+// (network.py:81-96, used as x @ W) into the device weight image: a constant
+// block (affine, biases, head) and one B operand block per GEMM, stored N x K
+// K-major in the UMMA canonical no-swizzle layout, split hi/lo for 3xTF32:
+// hi = rna_tf32(w), lo = rna_tf32(w - hi), both computed from the float64 weight.
+#include <cmath>
+#include <cstring>
+#include <vector>
 #include "tbn_tc.h"
+#include "tc_kernel.cuh"
 
 namespace tbn {
-bool tc_supported(const HostParams&, int) { return false; }
-bool tc_pack(const HostParams&, int, TcModel*, std::string* err) {
-  if (err) *err = "not built";
-  return false;
+
+namespace {
+
+float tf32_rna_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & 0xFFFFE000u;
+  float y;
+  std::memcpy(&y, &u, 4);
+  return y;
 }
-void tc_free(TcModel*) {}
-cudaError_t launch_tc(const TcModel&, const ForwardArgs&, int, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+// Pack W (Kin x N, row-major, x @ W) into B = W^T as N x Kp K-major canonical
+// blocks: float index (n/8)*(Kp*8) + (k/4)*32 + (n%8)*4 + (k%4).  Rows n >= Nvalid
+// and columns k >= Kin are zero.
+void pack_block(std::vector<float>& img, size_t off_floats, const double* W, int Kin, int Nvalid,
+                int N, int Kp, bool x3, int col_stride) {
+  float* hi = img.data() + off_floats;
+  float* lo = hi + (size_t)N * Kp;
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < Kp; ++k) {
+      const size_t idx = (size_t)(n / 8) * (Kp * 8) + (k / 4) * 32 + (n % 8) * 4 + (k % 4);
+      double w = (n < Nvalid && k < Kin) ? W[(size_t)k * col_stride + n] : 0.0;
+      float h = tf32_rna_host((float)w);
+      hi[idx] = h;
+      if (x3) lo[idx] = tf32_rna_host((float)(w - (double)h));
+    }
 }
+
+struct Instance {
+  int F, ND, NA, S, C, prec;
+  bool (*pack)(const HostParams&, TcModel*, std::string*);
+  cudaError_t (*launch)(const TcModel&, const ForwardArgs&, int, cudaStream_t);
+};
+
+template <class CF>
+bool pack_impl(const HostParams& hp, TcModel* out, std::string* err) {
+  constexpr int F = CF::F, H = CF::H, N2 = CF::N2, S = CF::S, ND = CF::ND, NA = CF::NA, C = CF::C;
+  std::vector<float> c(CF::C_END, 0.0f);
+  for (int f = 0; f < F; ++f) {
+    c[CF::C_SCALE + f] = (float)(1.0 / std::sqrt(hp.norm_var[f] + 1e-8));   // network.py:120
+    c[CF::C_SHIFT + f] = (float)hp.norm_mean[f];
+  }
+  for (int n = 0; n < N2; ++n) {
+    c[CF::C_BSH1 + n] = (float)hp.sh1_b[n];
+    c[CF::C_BSH2 + n] = (float)hp.sh2_b[n];
+    for (int s = 0; s <= S; ++s) {
+      c[CF::C_BFC1 + s * N2 + n] = (float)hp.fc1_b[s][n];
+      c[CF::C_BFC2 + s * N2 + n] = (float)hp.fc2_b[s][n];
+    }
+  }
+  for (int s = 1; s <= S; ++s)
+    for (int f = 0; f < F; ++f) c[CF::C_BATT + (s - 1) * CF::FN + f] = (float)hp.att_b[s][f];
+  for (int i = 0; i < ND * C; ++i) c[CF::C_HW + i] = (float)hp.head_W[i];
+  for (int i = 0; i < C; ++i) c[CF::C_HB + i] = (float)hp.head_b[i];
+
+  const size_t a16 = 16;
+  auto al = [&](size_t v) { return (v + a16 - 1) / a16 * a16; };
+  size_t off = al(CF::CONST_BYTES);
+  tc::TcParams tp{};
+  tp.off_sh1 = (uint32_t)off; off = al(off + CF::B_SH1);
+  tp.off_sh2 = (uint32_t)off; off = al(off + CF::B_HID);
+  tp.off_fc1 = (uint32_t)off; off = al(off + (size_t)(S + 1) * CF::B_HID);
+  tp.off_fc2 = (uint32_t)off; off = al(off + (size_t)(S + 1) * CF::B_HID);
+  tp.off_att = (uint32_t)off; off = al(off + (size_t)S * CF::B_ATT);
+  tp.gamma = (float)hp.gamma;
+  const size_t bytes = off;
+  std::vector<float> img(bytes / 4, 0.0f);
+  std::memcpy(img.data(), c.data(), c.size() * 4);
+  pack_block(img, tp.off_sh1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2);
+  pack_block(img, tp.off_sh2 / 4, hp.sh2_W, H, N2, N2, H, CF::X3, N2);
+  for (int s = 0; s <= S; ++s) {
+    pack_block(img, (tp.off_fc1 + (size_t)s * CF::B_HID) / 4, hp.fc1_W[s], H, N2, N2, H, CF::X3, N2);
+    pack_block(img, (tp.off_fc2 + (size_t)s * CF::B_HID) / 4, hp.fc2_W[s], H, N2, N2, H, CF::X3, N2);
+  }
+  for (int s = 1; s <= S; ++s)
+    pack_block(img, (tp.off_att + (size_t)(s - 1) * CF::B_ATT) / 4, hp.att_W[s], NA, F, CF::FN, NA,
+               CF::X3, F);
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (d) cudaFree(d);
+    if (err) *err = cudaGetErrorString(e);
+    return false;
+  }
+  tp.wimg = (const uint8_t*)d;
+  out->d_buf = d;
+  out->bytes = bytes;
+  out->params = new tc::TcParams(tp);
+  return true;
+}
+
+template <class CF>
+cudaError_t launch_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  static bool configured = false;
+  constexpr int smem = tc::Smem<CF>::TOTAL;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tc::tabnet_fused_tc<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const int64_t npairs = (ntiles + CF::NG - 1) / CF::NG;
+  const int grid = (int)(npairs < num_sms ? npairs : num_sms);
+  tc::tabnet_fused_tc<CF><<<grid, CF::THREADS, smem, stream>>>(*(const tc::TcParams*)m.params, a);
+  return cudaGetLastError();
+}
+
+#define TBN_INSTANCE(F, ND, NA, S, C, P)                                             \
+  Instance{F, ND, NA, S, C, P, &pack_impl<tc::Cfg<F, ND, NA, S, C, P>>,             \
+           &launch_impl<tc::Cfg<F, ND, NA, S, C, P>>}
+
+// Compiled model shapes (BASELINE.json configs; BLS as its 2-class reference model).
+const Instance kInstances[] = {
+    TBN_INSTANCE(14, 8, 8, 3, 2, tc::kPrecTF32x3),   // Adult
+    TBN_INSTANCE(14, 8, 8, 3, 2, tc::kPrecTF32),
+    TBN_INSTANCE(35, 16, 16, 5, 2, tc::kPrecTF32x3), // HR
+    TBN_INSTANCE(35, 16, 16, 5, 2, tc::kPrecTF32),
+    TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecTF32x3), // BLS
+    TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecTF32),
+};
+
+const Instance* find(const HostParams& hp, int precision) {
+  int prec = precision == 0 ? tc::kPrecTF32x3 : (precision == 1 ? tc::kPrecTF32 : -1);
+  for (const Instance& in : kInstances)
+    if (in.F == hp.F && in.ND == hp.ND && in.NA == hp.NA && in.S == hp.S && in.C == hp.C && in.prec == prec)
+      return &in;
+  return nullptr;
+}
+
+}  // namespace
+
+bool tc_supported(const HostParams& hp, int precision) { return find(hp, precision) != nullptr; }
+
+bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err) {
+  const Instance* in = find(hp, precision);
+  if (!in) {
+    if (err) *err = "no instance";
+    return false;
+  }
+  out->shape_id = (int)(in - kInstances);
+  out->precision = precision;
+  return in->pack(hp, out, err);
+}
+
+void tc_free(TcModel* m) {
+  if (m->d_buf) cudaFree(m->d_buf);
+  delete (tc::TcParams*)m->params;
+  m->d_buf = nullptr;
+  m->params = nullptr;
+}
+
+cudaError_t launch_tc(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  if (m.shape_id < 0) return cudaErrorInvalidValue;
+  return kInstances[m.shape_id].launch(m, a, num_sms, stream);
+}
+
 }  // namespace tbn

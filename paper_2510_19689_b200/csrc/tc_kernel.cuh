@@ -1,0 +1,691 @@
+// tc_kernel.cuh — K1: the whole TabNet forward (network.py:195-267) as ONE
+// persistent sm_100a kernel.  Row tiles of 128 (one row per epilogue thread,
+// one TMEM lane per row) stay on-chip for all decision steps:
+//
+//   TMEM (per row-group of 128 rows)      SMEM (per CTA)
+//   [D  accumulator, DW cols ]            consts: affine, biases, head
+//   [A  operand hi,  KA cols ]            resident shared1/shared2 (if they fit)
+//   [A  operand lo,  KA cols ] (3xTF32)   weight ring (per-step B operands, TMA bulk)
+//   [xn F][prior F][agg F]  per-row state x staging (TMA bulk, 1 tile ahead)
+//                                         [F][129] transpose buffer (coalesced I/O)
+//
+// Warp roles: NG row-groups x 4 epilogue warps (thread-per-row GLU / attentive /
+// sparsemax / aggregation math on CUDA cores), 1 MMA warp (a single thread
+// issues tcgen05.mma kind::tf32 with A from TMEM, B from SMEM), 1 producer warp
+// (cp.async.bulk of x tiles and weight blocks).  With NG = 2 the two row-groups
+// ping-pong: one group's epilogue overlaps the other group's MMAs.
+//
+// Per-row arithmetic is identical for every row whatever the batch size, tile
+// position, grid size or group: the batch-invariance contract (network.py:11-14).
+#pragma once
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+#include "tc_ptx.cuh"
+#include "tbn_internal.h"
+
+namespace tbn {
+namespace tc {
+
+constexpr int kPrecTF32x3 = 0;
+constexpr int kPrecTF32 = 1;
+
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
+constexpr int pow2ceil(int v) { int p = 32; while (p < v) p <<= 1; return p; }
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kR = 0.70710678118654752440f;   // sqrt(0.5), network.py:29
+
+template <int F_, int ND_, int NA_, int S_, int C_, int PREC_>
+struct Cfg {
+  static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
+  static constexpr int H = ND + NA, N2 = 2 * H;
+  static constexpr bool X3 = (PREC == kPrecTF32x3);
+  static constexpr int K1 = rup(F, 8);                 // shared1 K (tf32 granule 8)
+  static constexpr int FN = rup(F, 16);                // attentive N (M=128 needs N%16==0)
+  static constexpr int KA = cmax(cmax(K1, H), NA);     // A operand columns
+  static constexpr int DW = cmax(N2, FN);              // accumulator columns
+  // TMEM column map (per group)
+  static constexpr int T_D = 0, T_A = DW, T_AL = T_A + KA, T_XN = T_AL + (X3 ? KA : 0);
+  static constexpr int T_PR = T_XN + F, T_AG = T_PR + F, T_END = T_AG + F;
+  static constexpr int TCOLS_G = pow2ceil(T_END);
+  static constexpr int NG = (2 * TCOLS_G <= 512) ? 2 : 1;
+  static constexpr int TCOLS = NG * TCOLS_G;
+  static_assert(TCOLS <= 512, "per-row state does not fit in TMEM");
+  static_assert(N2 <= 256 && FN <= 256, "MMA N > 256");
+  // weight blocks (B operands, K-major canonical, hi [+ lo])
+  static constexpr int PARTS = X3 ? 2 : 1;
+  static constexpr int B_SH1 = PARTS * N2 * K1 * 4;
+  static constexpr int B_HID = PARTS * N2 * H * 4;     // shared2, fc1_s, fc2_s
+  static constexpr int B_ATT = PARTS * FN * NA * 4;
+  // consts (floats): scale F | shift F | bias sh1 N2 | sh2 N2 | fc1 (S+1)N2 | fc2 (S+1)N2 |
+  //                  att S*FN | head_W ND*C | head_b C
+  static constexpr int C_SCALE = 0, C_SHIFT = C_SCALE + rup(F, 4), C_BSH1 = C_SHIFT + rup(F, 4);
+  static constexpr int C_BSH2 = C_BSH1 + N2, C_BFC1 = C_BSH2 + N2, C_BFC2 = C_BFC1 + (S + 1) * N2;
+  static constexpr int C_BATT = C_BFC2 + (S + 1) * N2, C_HW = C_BATT + S * FN;
+  static constexpr int C_HB = C_HW + rup(ND * C, 4), C_END = rup(C_HB + C, 4);
+  static constexpr int CONST_BYTES = C_END * 4;
+  // shared-memory plan
+  static constexpr int XSTAGE = rup(128 * F * 4, 128);
+  static constexpr int TSTAGE = rup(F * 129 * 4, 128);
+  static constexpr int FIXED = rup(CONST_BYTES, 128) + NG * (XSTAGE + TSTAGE) + 1024;
+  static constexpr int RING_SLOT_ALL = cmax(cmax(B_SH1, B_HID), B_ATT);
+  static constexpr int RING_SLOT_RES = cmax(B_HID, B_ATT);
+  static constexpr int SMEM_BUDGET = 225 * 1024;
+  static constexpr bool RESIDENT = FIXED + B_SH1 + B_HID + 3 * RING_SLOT_RES <= SMEM_BUDGET;
+  static constexpr int SLOT = RESIDENT ? RING_SLOT_RES : RING_SLOT_ALL;
+  static constexpr int NSLOT = RESIDENT ? 3 : ((FIXED + 3 * SLOT <= SMEM_BUDGET) ? 3 : 2);
+  static constexpr int RES_BYTES = RESIDENT ? (B_SH1 + B_HID) : 0;
+  static constexpr int SMEM_BYTES = FIXED + RES_BYTES + NSLOT * SLOT;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared-memory plan exceeds 227 KB");
+  // GEMMs per tile: step 0 transform (4) + S x (att + transform 4)
+  static constexpr int GEMMS = 4 + 5 * S;
+  static constexpr int THREADS = NG * 128 + 64;
+};
+
+// Global-memory weight image (built by the host packer, tc_pack):
+//   [consts][sh1 blk][sh2 blk][fc1_0..fc1_S blks][fc2_0..fc2_S blks][att_1..att_S blks]
+struct TcParams {
+  const uint8_t* wimg;     // device image
+  uint32_t off_sh1, off_sh2, off_fc1, off_fc2, off_att;   // byte offsets of block 0 of each kind
+  float gamma;
+};
+
+// ---- TMEM <-> registers helpers over an exact column count (any N) ----------
+template <int N, int OFF = 0, int M>
+__device__ __forceinline__ void tmem_load_n(uint32_t taddr, float (&v)[M]) {
+  if constexpr (N >= 16) {
+    uint32_t r[16];
+    TBN_TMEM_LD16(taddr, r);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[OFF + i] = __uint_as_float(r[i]);
+    tmem_load_n<N - 16, OFF + 16>(taddr + 16, v);
+  } else if constexpr (N >= 8) {
+    uint32_t r[8];
+    TBN_TMEM_LD8(taddr, r);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[OFF + i] = __uint_as_float(r[i]);
+    tmem_load_n<N - 8, OFF + 8>(taddr + 8, v);
+  } else if constexpr (N >= 4) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(taddr));
+    v[OFF] = __uint_as_float(r0); v[OFF + 1] = __uint_as_float(r1);
+    v[OFF + 2] = __uint_as_float(r2); v[OFF + 3] = __uint_as_float(r3);
+    tmem_load_n<N - 4, OFF + 4>(taddr + 4, v);
+  } else if constexpr (N >= 2) {
+    uint32_t r0, r1;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(taddr));
+    v[OFF] = __uint_as_float(r0); v[OFF + 1] = __uint_as_float(r1);
+    tmem_load_n<N - 2, OFF + 2>(taddr + 2, v);
+  } else if constexpr (N == 1) {
+    uint32_t r0;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r0) : "r"(taddr));
+    v[OFF] = __uint_as_float(r0);
+  }
+}
+
+template <int N, int OFF = 0, int M>
+__device__ __forceinline__ void tmem_store_n(uint32_t taddr, const float (&v)[M]) {
+  if constexpr (N >= 16) {
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(v[OFF + i]);
+    TBN_TMEM_ST16(taddr, r);
+    tmem_store_n<N - 16, OFF + 16>(taddr + 16, v);
+  } else if constexpr (N >= 8) {
+    uint32_t r[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(v[OFF + i]);
+    TBN_TMEM_ST8(taddr, r);
+    tmem_store_n<N - 8, OFF + 8>(taddr + 8, v);
+  } else if constexpr (N >= 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[OFF])), "r"(__float_as_uint(v[OFF + 1])),
+                 "r"(__float_as_uint(v[OFF + 2])), "r"(__float_as_uint(v[OFF + 3])));
+    tmem_store_n<N - 4, OFF + 4>(taddr + 4, v);
+  } else if constexpr (N >= 2) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[OFF])), "r"(__float_as_uint(v[OFF + 1])));
+    tmem_store_n<N - 2, OFF + 2>(taddr + 2, v);
+  } else if constexpr (N == 1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[OFF])));
+  }
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Round-to-nearest (ties away) to TF32 on the bit pattern: the result has its
+// 13 low mantissa bits zero, so the tensor core's operand truncation is exact.
+__device__ __forceinline__ float tf32_rna(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// Compile-time loop over [0, N) in chunks of CH columns: fn(integral_constant<O>, integral_constant<L>).
+template <int N, int CH = 16, int O = 0, class Fn>
+__device__ __forceinline__ void chunked(Fn&& fn) {
+  if constexpr (O < N) {
+    constexpr int L = (N - O < CH) ? (N - O) : CH;
+    fn(std::integral_constant<int, O>{}, std::integral_constant<int, L>{});
+    chunked<N, CH, O + L>(fn);
+  }
+}
+
+// Write L columns of an A operand row to TMEM: hi = rna_tf32(v), lo = v - hi
+// (3xTF32), or v as is (the tensor core truncates fp32 to tf32).
+template <class CF, int L, int M>
+__device__ __forceinline__ void store_a(uint32_t t_a, uint32_t t_al, const float (&v)[M]) {
+  if constexpr (CF::X3) {
+    float hi[L], lo[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      hi[i] = tf32_rna(v[i]);
+      lo[i] = v[i] - hi[i];
+    }
+    tmem_store_n<L>(t_a, hi);
+    tmem_store_n<L>(t_al, lo);
+  } else {
+    tmem_store_n<L>(t_a, v);
+  }
+}
+// A <- v[0..K) in 16-column chunks
+template <class CF, int K, int M>
+__device__ __forceinline__ void store_a_all(uint32_t t_a, uint32_t t_al, const float (&v)[M]) {
+  chunked<K>([&](auto o, auto l) {
+    constexpr int O = decltype(o)::value, L = decltype(l)::value;
+    float c[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) c[i] = v[O + i];
+    store_a<CF, L>(t_a + O, t_al + O, c);
+  });
+}
+
+// ---------------------------------------------------------------------------
+template <class CF>
+struct Smem {
+  static constexpr int OFF_CONST = 0;
+  static constexpr int OFF_X = rup(CF::CONST_BYTES, 128);
+  static constexpr int OFF_T = OFF_X + CF::NG * CF::XSTAGE;
+  static constexpr int OFF_RES = rup(OFF_T + CF::NG * CF::TSTAGE, 1024);
+  static constexpr int OFF_RING = OFF_RES + CF::RES_BYTES;
+  static constexpr int OFF_BAR = OFF_RING + CF::NSLOT * CF::SLOT;
+  static constexpr int TOTAL = OFF_BAR + 256;
+  static_assert(TOTAL <= 227 * 1024, "smem");
+};
+
+struct Bars {
+  uint64_t wfull[4];
+  uint64_t wempty[4];
+  uint64_t xfull[2];
+  uint64_t xempty[2];
+  uint64_t afull[2];
+  uint64_t dfull[2];
+  uint64_t cfull;
+  uint32_t tmem_base;
+};
+
+// The weight-block sequence of one tile pair: index j in [0, GEMMS)
+//   j = 0..3          : sh1, sh2, fc1_0, fc2_0
+//   j = 4 + 5(s-1) + 0: att_s ; +1..+4: sh1, sh2, fc1_s, fc2_s   (s = 1..S)
+// kind: 0 sh1, 1 sh2, 2 fc1, 3 fc2, 4 att
+__device__ __forceinline__ void gemm_of(int j, int& kind, int& step) {
+  if (j < 4) { kind = j; step = 0; return; }
+  int q = j - 4;
+  step = q / 5 + 1;
+  int r = q % 5;
+  kind = (r == 0) ? 4 : r - 1;
+}
+
+template <class CF>
+__device__ __forceinline__ uint32_t block_offset(const TcParams& p, int kind, int step) {
+  switch (kind) {
+    case 0: return p.off_sh1;
+    case 1: return p.off_sh2;
+    case 2: return p.off_fc1 + (uint32_t)step * CF::B_HID;
+    case 3: return p.off_fc2 + (uint32_t)step * CF::B_HID;
+    default: return p.off_att + (uint32_t)(step - 1) * CF::B_ATT;
+  }
+}
+template <class CF>
+__device__ __forceinline__ uint32_t block_bytes(int kind) {
+  return kind == 0 ? CF::B_SH1 : (kind == 4 ? CF::B_ATT : CF::B_HID);
+}
+template <class CF>
+__device__ __forceinline__ bool is_resident(int kind) {
+  return CF::RESIDENT && (kind == 0 || kind == 1);
+}
+
+// ---------------------------------------------------------------------------
+template <class CF>
+__global__ void __launch_bounds__(CF::THREADS, 1)
+tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  using SM = Smem<CF>;
+  constexpr int F = CF::F, H = CF::H, ND = CF::ND, NA = CF::NA, S = CF::S, C = CF::C, NG = CF::NG;
+  const float* cst = reinterpret_cast<const float*>(smem + SM::OFF_CONST);
+  Bars* bars = reinterpret_cast<Bars*>(smem + SM::OFF_BAR);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const int64_t npairs = (ntiles + NG - 1) / NG;
+  const bool x_bulk_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0);
+
+  // ---- setup ----
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < CF::NSLOT; ++i) { ptx::mbar_init(&bars->wfull[i], 1); ptx::mbar_init(&bars->wempty[i], 1); }
+    for (int g = 0; g < NG; ++g) {
+      ptx::mbar_init(&bars->xfull[g], 1);
+      ptx::mbar_init(&bars->xempty[g], 128);
+      ptx::mbar_init(&bars->afull[g], 128);
+      ptx::mbar_init(&bars->dfull[g], 1);
+    }
+    ptx::mbar_init(&bars->cfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc<CF::TCOLS>(&bars->tmem_base);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = bars->tmem_base;
+
+  const int producer_warp = NG * 4 + 1, mma_warp = NG * 4;
+
+  if (warp == producer_warp) {
+    // ======================= PRODUCER (TMA bulk copies) =======================
+    if (ptx::elect_one()) {
+      uint32_t cbytes = CF::CONST_BYTES + CF::RES_BYTES;
+      ptx::mbar_arrive_expect_tx(&bars->cfull, cbytes);
+      ptx::bulk_g2s(smem + SM::OFF_CONST, p.wimg, CF::CONST_BYTES, &bars->cfull);
+      if constexpr (CF::RESIDENT) {
+        ptx::bulk_g2s(smem + SM::OFF_RES, p.wimg + p.off_sh1, CF::B_SH1, &bars->cfull);
+        ptx::bulk_g2s(smem + SM::OFF_RES + CF::B_SH1, p.wimg + p.off_sh2, CF::B_HID, &bars->cfull);
+      }
+      uint32_t xphase[2] = {0, 0};
+      auto load_x = [&](int64_t pair) {
+        for (int g = 0; g < NG; ++g) {
+          int64_t tile = pair * NG + g;
+          if (tile >= ntiles) continue;
+          ptx::mbar_wait(&bars->xempty[g], xphase[g] ^ 1);
+          xphase[g] ^= 1;
+          int64_t r0 = tile * 128;
+          int64_t nr = a.rows - r0 < 128 ? a.rows - r0 : 128;
+          uint32_t bytes = x_bulk_ok ? (uint32_t)((nr * F * 4) & ~15ll) : 0u;
+          if (bytes) {
+            ptx::mbar_arrive_expect_tx(&bars->xfull[g], bytes);
+            ptx::bulk_g2s(smem + SM::OFF_X + g * CF::XSTAGE, a.x + r0 * F, bytes, &bars->xfull[g]);
+          } else {
+            ptx::mbar_arrive(&bars->xfull[g]);
+          }
+        }
+      };
+      int slot = 0;
+      uint32_t wphase = 0;
+      int64_t pair = blockIdx.x;
+      if (pair < npairs) load_x(pair);
+      for (; pair < npairs; pair += gridDim.x) {
+        for (int j = 0; j < CF::GEMMS; ++j) {
+          int kind, step;
+          gemm_of(j, kind, step);
+          if (j == 2 && pair + gridDim.x < npairs) load_x(pair + gridDim.x);   // prefetch next tiles
+          if (is_resident<CF>(kind)) continue;
+          ptx::mbar_wait(&bars->wempty[slot], wphase ^ 1);
+          uint32_t bytes = block_bytes<CF>(kind);
+          ptx::mbar_arrive_expect_tx(&bars->wfull[slot], bytes);
+          ptx::bulk_g2s(smem + SM::OFF_RING + slot * CF::SLOT, p.wimg + block_offset<CF>(p, kind, step),
+                        bytes, &bars->wfull[slot]);
+          if (++slot == CF::NSLOT) { slot = 0; wphase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == mma_warp) {
+    // ======================= MMA ISSUER (one thread) ===========================
+    if (ptx::elect_one()) {
+      ptx::mbar_wait(&bars->cfull, 0);
+      uint32_t aphase[2] = {0, 0};
+      int slot = 0;
+      uint32_t wphase = 0;
+      for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
+        for (int j = 0; j < CF::GEMMS; ++j) {
+          int kind, step;
+          gemm_of(j, kind, step);
+          const bool res = is_resident<CF>(kind);
+          uint32_t bsm;
+          if (res) {
+            bsm = ptx::smem_u32(smem + SM::OFF_RES + (kind == 0 ? 0 : CF::B_SH1));
+          } else {
+            ptx::mbar_wait(&bars->wfull[slot], wphase);
+            bsm = ptx::smem_u32(smem + SM::OFF_RING + slot * CF::SLOT);
+          }
+          const int K = kind == 0 ? CF::K1 : (kind == 4 ? NA : H);
+          const int N = kind == 4 ? CF::FN : CF::N2;
+          const uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtTF32, 128, N);
+          const uint32_t sbo = (uint32_t)(K / 4) * 128u;
+          const uint32_t lo_off = (uint32_t)(N * K * 4);
+          for (int g = 0; g < NG; ++g) {
+            if (pair * NG + g >= ntiles) continue;
+            ptx::mbar_wait(&bars->afull[g], aphase[g]);
+            aphase[g] ^= 1;
+            ptx::tc_fence_after();
+            const uint32_t tg = tbase + (uint32_t)(g * CF::TCOLS_G);
+            for (int k0 = 0; k0 < K; k0 += 8) {
+              const uint64_t bd = ptx::smem_desc(bsm + (uint32_t)k0 * 32u, 128u, sbo);
+              ptx::mma_tf32_ts(tg + CF::T_D, tg + CF::T_A + k0, bd, idesc, k0 > 0 ? 1u : 0u);
+              if constexpr (CF::X3) {
+                const uint64_t bdl = ptx::smem_desc(bsm + lo_off + (uint32_t)k0 * 32u, 128u, sbo);
+                ptx::mma_tf32_ts(tg + CF::T_D, tg + CF::T_AL + k0, bd, idesc, 1u);
+                ptx::mma_tf32_ts(tg + CF::T_D, tg + CF::T_A + k0, bdl, idesc, 1u);
+              }
+            }
+            ptx::mma_commit(&bars->dfull[g]);
+          }
+          if (!res) {
+            ptx::mma_commit(&bars->wempty[slot]);
+            if (++slot == CF::NSLOT) { slot = 0; wphase ^= 1; }
+          }
+        }
+      }
+    }
+  } else {
+    // ======================= EPILOGUE / ROW MATH (thread = row) =================
+    const int g = warp >> 2;                 // row group
+    const int t = threadIdx.x & 127;         // row within tile == TMEM lane
+    const uint32_t tg = tbase + (uint32_t)(g * CF::TCOLS_G) + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t tD = tg + CF::T_D, tA = tg + CF::T_A, tAL = tg + CF::T_AL;
+    const uint32_t tXN = tg + CF::T_XN, tPR = tg + CF::T_PR, tAG = tg + CF::T_AG;
+    const float* xs = reinterpret_cast<const float*>(smem + SM::OFF_X + g * CF::XSTAGE);
+    float* ts = reinterpret_cast<float*>(smem + SM::OFF_T + g * CF::TSTAGE);
+    const uint32_t bar_id = 1 + g;
+    ptx::mbar_wait(&bars->cfull, 0);
+    const float* scale = a.scale ? a.scale : cst + CF::C_SCALE;
+    const float* shift = a.shift ? a.shift : cst + CF::C_SHIFT;
+    uint32_t xphase = 0, dphase = 0;
+
+    auto arrive_a = [&]() {
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&bars->afull[g]);
+    };
+    auto wait_d = [&]() {
+      ptx::mbar_wait(&bars->dfull[g], dphase);
+      dphase ^= 1;
+      ptx::tc_fence_after();
+    };
+    // GLU block epilogue: D -> g (+ residual), prev updated; bias from consts.
+    // u = D + b; out = u_lin * sigmoid(u_gate) [; out = (out + prev) * sqrt(.5)]
+    auto glu = [&](const float* b, bool residual, float (&prev)[H]) {
+#pragma unroll
+      for (int j0 = 0; j0 < H; j0 += 8) {
+        float lin[8], gate[8];
+        tmem_load_n<8>(tD + j0, lin);
+        tmem_load_n<8>(tD + H + j0, gate);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float ug = gate[i] + b[H + j0 + i];
+          const float e = ex2_approx(-ug * kLog2e);
+          const float v = (lin[i] + b[j0 + i]) * rcp_approx(1.0f + e);
+          prev[j0 + i] = residual ? (v + prev[j0 + i]) * kR : v;
+        }
+      }
+    };
+
+    for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
+      const int64_t tile = pair * NG + g;
+      if (tile >= ntiles) continue;
+      const int64_t r0 = tile * 128;
+      const int nrows = (int)(a.rows - r0 < 128 ? a.rows - r0 : 128);
+      const bool valid = t < nrows;
+      const int64_t row = r0 + t;
+
+      // ---- x tile: staging (TMA) -> [F][129] transpose -> per-row normalize ----
+      ptx::mbar_wait(&bars->xfull[g], xphase);
+      xphase ^= 1;
+      {
+        const int ne = nrows * F;
+        const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
+        ptx::named_bar_sync(bar_id, 128);   // previous tile's readers of ts are done
+        for (int e = t; e < 128 * F; e += 128) {
+          float v = 0.0f;
+          if (e < nbulk) v = xs[e];
+          else if (e < ne) v = a.x[r0 * F + e];
+          const int rr = e / F, ff = e - rr * F;
+          ts[ff * 129 + rr] = v;
+        }
+        ptx::named_bar_sync(bar_id, 128);
+        ptx::mbar_arrive(&bars->xempty[g]);  // staging buffer may be refilled
+      }
+      // xn = (x - mean) * rsqrt(var + eps) (network.py:118-120); prior = 1; agg = 0
+      {
+        int bad = 0;
+        chunked<CF::K1>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          float xn[L], one[L], zero[L];
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            const int f = O + i;
+            one[i] = 1.0f;
+            zero[i] = 0.0f;
+            if (f < F) {
+              const float xv = ts[f * 129 + t];
+              bad |= !isfinite(xv);
+              xn[i] = a.normalized ? xv : (xv - shift[f]) * scale[f];
+            } else {
+              xn[i] = 0.0f;
+            }
+          }
+          constexpr int LF = (O + L <= F) ? L : (O < F ? F - O : 0);
+          if constexpr (LF > 0) {
+            tmem_store_n<LF>(tXN + O, xn);
+            tmem_store_n<LF>(tPR + O, one);
+            tmem_store_n<LF>(tAG + O, zero);
+          }
+          store_a<CF, L>(tA + O, tAL + O, xn);
+        });
+        if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
+        arrive_a();
+      }
+      float prev[H];
+      float dsum[ND];
+#pragma unroll
+      for (int j = 0; j < ND; ++j) dsum[j] = 0.0f;
+      bool all_eta_zero = true;
+
+      // feature transformer (network.py:124-141): 4 GEMM+GLU blocks
+      auto transform = [&](int step) {
+        wait_d();
+        glu(cst + CF::C_BSH1, false, prev);                          // g1 = GLU(u1)
+        store_a_all<CF, H>(tA, tAL, prev);
+        arrive_a();
+        wait_d();
+        glu(cst + CF::C_BSH2, true, prev);                           // g2
+        store_a_all<CF, H>(tA, tAL, prev);
+        arrive_a();
+        wait_d();
+        glu(cst + CF::C_BFC1 + step * CF::N2, true, prev);           // g3
+        store_a_all<CF, H>(tA, tAL, prev);
+        arrive_a();
+        wait_d();
+        glu(cst + CF::C_BFC2 + step * CF::N2, true, prev);           // g4 = f
+      };
+
+      transform(0);                                                   // network.py:226-227
+      for (int s = 1; s <= S; ++s) {
+        // A <- a = f[:, n_d:]
+        {
+          float av[NA];
+#pragma unroll
+          for (int k = 0; k < NA; ++k) av[k] = prev[ND + k];
+          store_a_all<CF, NA>(tA, tAL, av);
+          arrive_a();
+        }
+        // attentive FC + prior + sparsemax (network.py:233-236, sparsemax.py:13-41)
+        wait_d();
+        float z[F];
+        const float* batt = cst + CF::C_BATT + (s - 1) * CF::FN;
+        float zmax = -INFINITY;
+        chunked<F>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          float pr[L];
+          tmem_load_n<L, O>(tD + O, z);
+          tmem_load_n<L>(tPR + O, pr);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            z[O + i] = pr[i] * (z[O + i] + batt[O + i]);            // network.py:233-235
+            zmax = fmaxf(zmax, z[O + i]);
+          }
+        });
+#pragma unroll
+        for (int f = 0; f < F; ++f) z[f] -= zmax;                     // sparsemax.py:32
+        float tau = -1.0f;
+        int cnt_prev = F + 1;
+        for (int it = 0; it <= F; ++it) {                             // sort-free support search
+          float sm = 0.0f;
+          int c = 0;
+#pragma unroll
+          for (int f = 0; f < F; ++f)
+            if (z[f] > tau) { sm += z[f]; ++c; }
+          if (c >= cnt_prev) break;
+          cnt_prev = c;
+          tau = __fdiv_rn(sm - 1.0f, (float)c);                       // sparsemax.py:39
+        }
+        ptx::named_bar_sync(bar_id, 128);    // previous readers of ts are done
+        chunked<CF::K1>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          constexpr int LF = (O + L <= F) ? L : (O < F ? F - O : 0);
+          float pr[L], xnv[L], xm[L];
+          if constexpr (LF > 0) {
+            tmem_load_n<LF>(tPR + O, pr);
+            tmem_load_n<LF>(tXN + O, xnv);
+            ptx::tmem_ld_wait();
+          }
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            const int f = O + i;
+            if (f < F) {
+              const float m = fmaxf(z[f] - tau, 0.0f);                // sparsemax.py:40
+              pr[i] = pr[i] * (p.gamma - m);                          // network.py:237
+              xm[i] = m * xnv[i];                                     // network.py:238
+              ts[f * 129 + t] = m;
+            } else {
+              xm[i] = 0.0f;
+            }
+          }
+          if constexpr (LF > 0) tmem_store_n<LF>(tPR + O, pr);
+          store_a<CF, L>(tA + O, tAL + O, xm);
+        });
+        arrive_a();
+        ptx::named_bar_sync(bar_id, 128);
+        // masks[s-1] tile: coalesced store from the [F][129] buffer (network.py:246)
+        if (a.masks) {
+          float* dst = a.masks + ((int64_t)(s - 1) * a.rows + r0) * F;
+          for (int e = t; e < nrows * F; e += 128) {
+            const int rr = e / F, ff = e - rr * F;
+            dst[e] = ts[ff * 129 + rr];
+          }
+        }
+        transform(s);
+        // d = relu(f[:, :n_d]); d_sum += d; eta = sum(d); agg += eta*m (network.py:241-245)
+        float eta = 0.0f;
+#pragma unroll
+        for (int j = 0; j < ND; ++j) {
+          const float d = fmaxf(prev[j], 0.0f);
+          dsum[j] += d;
+          eta += d;
+        }
+        // While every eta so far is 0, agg holds sum_s m instead (it is needed only
+        // for the importance fallback, network.py:259-261, which fires exactly then);
+        // the first eta > 0 resets it to eta*m, identical to the reference's sum.
+        const bool reset = all_eta_zero && eta > 0.0f;
+        const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
+        all_eta_zero = all_eta_zero && !(eta > 0.0f);
+        chunked<F>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          float ag[L];
+          tmem_load_n<L>(tAG + O, ag);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            const float base = reset ? 0.0f : ag[i];
+            ag[i] = fmaf(w, ts[(O + i) * 129 + t], base);
+          }
+          tmem_store_n<L>(tAG + O, ag);
+        });
+      }
+      // ---- head + softmax + argmax (network.py:253-256, :279) ----
+      {
+        float lg[C];
+        float lmax = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int k = 0; k < ND; ++k) acc = fmaf(dsum[k], cst[CF::C_HW + k * C + c], acc);
+          lg[c] = acc + cst[CF::C_HB + c];
+          lmax = fmaxf(lmax, lg[c]);
+        }
+        float ex[C], es = 0.0f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) { ex[c] = expf(lg[c] - lmax); es += ex[c]; }
+        int best = 0;
+        float bv = -1.0f;
+        if (valid) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const float pv = ex[c] / es;
+            if (a.logits) a.logits[row * C + c] = lg[c];
+            if (a.probs) a.probs[row * C + c] = pv;
+            if (pv > bv) { bv = pv; best = c; }
+          }
+          if (a.pred) a.pred[row] = best;
+        }
+      }
+      // ---- importance = agg / sum(agg), or mean_s(masks) (network.py:258-261) ----
+      {
+        float tot = 0.0f;
+        chunked<F>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          float ag[L];
+          tmem_load_n<L>(tAG + O, ag);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < L; ++i) tot += ag[i];
+        });
+        ptx::named_bar_sync(bar_id, 128);     // mask readers of ts are done
+        const float div = all_eta_zero ? (float)S : tot;
+        chunked<F>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          float ag[L];
+          tmem_load_n<L>(tAG + O, ag);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < L; ++i) ts[(O + i) * 129 + t] = ag[i] / div;
+        });
+        ptx::named_bar_sync(bar_id, 128);
+        if (a.importance) {
+          float* dst = a.importance + r0 * F;
+          for (int e = t; e < nrows * F; e += 128) {
+            const int rr = e / F, ff = e - rr * F;
+            dst[e] = ts[ff * 129 + rr];
+          }
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc<CF::TCOLS>(tbase);
+}
+
+}  // namespace tc
+}  // namespace tbn

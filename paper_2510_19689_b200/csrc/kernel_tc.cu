@@ -27,13 +27,14 @@ float tf32_rna_host(float x) {
 // blocks: float index (n/8)*(Kp*8) + (k/4)*32 + (n%8)*4 + (k%4).  Rows n >= Nvalid
 // and columns k >= Kin are zero.
 void pack_block(std::vector<float>& img, size_t off_floats, const double* W, int Kin, int Nvalid,
-                int N, int Kp, bool x3, int col_stride) {
+                int N, int Kp, bool x3, int col_stride, const std::vector<double>* colscale = nullptr) {
   float* hi = img.data() + off_floats;
   float* lo = hi + (size_t)N * Kp;
   for (int n = 0; n < N; ++n)
     for (int k = 0; k < Kp; ++k) {
       const size_t idx = (size_t)(n / 8) * (Kp * 8) + (k / 4) * 32 + (n % 8) * 4 + (k % 4);
       double w = (n < Nvalid && k < Kin) ? W[(size_t)k * col_stride + n] : 0.0;
+      if (colscale) w *= (*colscale)[n];
       float h = tf32_rna_host((float)w);
       hi[idx] = h;
       if (x3) lo[idx] = tf32_rna_host((float)(w - (double)h));
@@ -54,12 +55,22 @@ bool pack_impl(const HostParams& hp, TcModel* out, std::string* err) {
     c[CF::C_SCALE + f] = (float)(1.0 / std::sqrt(hp.norm_var[f] + 1e-8));   // network.py:120
     c[CF::C_SHIFT + f] = (float)hp.norm_mean[f];
   }
+  // Folded GLU constants (the epilogue in tc_kernel.cuh relies on them):
+  // gate columns x -log2(e) so exp(-u_gate) = 2^(D_gate + b'); the linear
+  // columns of the residual blocks (shared2, fc1, fc2) x sqrt(.5), so
+  // (lin*sigma + prev)*sqrt(.5) = lin'*sigma + sqrt(.5)*prev (network.py:131-137).
+  const double kLog2e = 1.4426950408889634, kR = 0.70710678118654752440;
+  std::vector<double> cs_first(N2), cs_res(N2);
   for (int n = 0; n < N2; ++n) {
-    c[CF::C_BSH1 + n] = (float)hp.sh1_b[n];
-    c[CF::C_BSH2 + n] = (float)hp.sh2_b[n];
+    cs_first[n] = n < H ? 1.0 : -kLog2e;
+    cs_res[n] = n < H ? kR : -kLog2e;
+  }
+  for (int n = 0; n < N2; ++n) {
+    c[CF::C_BSH1 + n] = (float)(hp.sh1_b[n] * cs_first[n]);
+    c[CF::C_BSH2 + n] = (float)(hp.sh2_b[n] * cs_res[n]);
     for (int s = 0; s <= S; ++s) {
-      c[CF::C_BFC1 + s * N2 + n] = (float)hp.fc1_b[s][n];
-      c[CF::C_BFC2 + s * N2 + n] = (float)hp.fc2_b[s][n];
+      c[CF::C_BFC1 + s * N2 + n] = (float)(hp.fc1_b[s][n] * cs_res[n]);
+      c[CF::C_BFC2 + s * N2 + n] = (float)(hp.fc2_b[s][n] * cs_res[n]);
     }
   }
   for (int s = 1; s <= S; ++s)
@@ -80,11 +91,11 @@ bool pack_impl(const HostParams& hp, TcModel* out, std::string* err) {
   const size_t bytes = off;
   std::vector<float> img(bytes / 4, 0.0f);
   std::memcpy(img.data(), c.data(), c.size() * 4);
-  pack_block(img, tp.off_sh1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2);
-  pack_block(img, tp.off_sh2 / 4, hp.sh2_W, H, N2, N2, H, CF::X3, N2);
+  pack_block(img, tp.off_sh1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first);
+  pack_block(img, tp.off_sh2 / 4, hp.sh2_W, H, N2, N2, H, CF::X3, N2, &cs_res);
   for (int s = 0; s <= S; ++s) {
-    pack_block(img, (tp.off_fc1 + (size_t)s * CF::B_HID) / 4, hp.fc1_W[s], H, N2, N2, H, CF::X3, N2);
-    pack_block(img, (tp.off_fc2 + (size_t)s * CF::B_HID) / 4, hp.fc2_W[s], H, N2, N2, H, CF::X3, N2);
+    pack_block(img, (tp.off_fc1 + (size_t)s * CF::B_HID) / 4, hp.fc1_W[s], H, N2, N2, H, CF::X3, N2, &cs_res);
+    pack_block(img, (tp.off_fc2 + (size_t)s * CF::B_HID) / 4, hp.fc2_W[s], H, N2, N2, H, CF::X3, N2, &cs_res);
   }
   for (int s = 1; s <= S; ++s)
     pack_block(img, (tp.off_att + (size_t)(s - 1) * CF::B_ATT) / 4, hp.att_W[s], NA, F, CF::FN, NA,

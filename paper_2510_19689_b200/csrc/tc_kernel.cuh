@@ -67,8 +67,12 @@ struct Cfg {
   static constexpr int C_HB = C_HW + rup(ND * C, 4), C_END = rup(C_HB + C, 4);
   static constexpr int CONST_BYTES = C_END * 4;
   // shared-memory plan
+  // Row I/O: thread-per-row reads/writes of a dense [128][F] tile are bank-
+  // conflict-free for odd F (and cheap for small F); otherwise go through a
+  // [F][129] transpose buffer with cooperative coalesced global accesses.
+  static constexpr bool DENSE_IO = (F % 2 == 1) || (F <= 16);
   static constexpr int XSTAGE = rup(128 * F * 4, 128);
-  static constexpr int TSTAGE = rup(F * 129 * 4, 128);
+  static constexpr int TSTAGE = DENSE_IO ? rup(128 * F * 4, 128) : rup(F * 129 * 4, 128);
   static constexpr int FIXED = rup(CONST_BYTES, 128) + NG * (XSTAGE + TSTAGE) + 1024;
   static constexpr int RING_SLOT_ALL = cmax(cmax(B_SH1, B_HID), B_ATT);
   static constexpr int RING_SLOT_RES = cmax(B_HID, B_ATT);
@@ -181,6 +185,8 @@ __device__ __forceinline__ void chunked(Fn&& fn) {
   }
 }
 
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
 // Write L columns of an A operand row to TMEM: hi = rna_tf32(v), lo = v - hi
 // (3xTF32), or v as is (the tensor core truncates fp32 to tf32).
 template <class CF, int L, int M>
@@ -188,10 +194,14 @@ __device__ __forceinline__ void store_a(uint32_t t_a, uint32_t t_al, const float
   if constexpr (CF::X3) {
     float hi[L], lo[L];
 #pragma unroll
-    for (int i = 0; i < L; ++i) {
-      hi[i] = tf32_rna(v[i]);
-      lo[i] = v[i] - hi[i];
+    for (int i = 0; i < L; ++i) hi[i] = tf32_rna(v[i]);
+#pragma unroll
+    for (int i = 0; i + 1 < L; i += 2) {
+      const float2 d = __fadd2_rn(f2(v[i], v[i + 1]), f2(-hi[i], -hi[i + 1]));
+      lo[i] = d.x;
+      lo[i + 1] = d.y;
     }
+    if constexpr (L % 2) lo[L - 1] = v[L - 1] - hi[L - 1];
     tmem_store_n<L>(t_a, hi);
     tmem_store_n<L>(t_al, lo);
   } else {
@@ -404,6 +414,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     const float* xs = reinterpret_cast<const float*>(smem + SM::OFF_X + g * CF::XSTAGE);
     float* ts = reinterpret_cast<float*>(smem + SM::OFF_T + g * CF::TSTAGE);
     const uint32_t bar_id = 1 + g;
+    const bool leader = (t == 0);
     ptx::mbar_wait(&bars->cfull, 0);
     const float* scale = a.scale ? a.scale : cst + CF::C_SCALE;
     const float* shift = a.shift ? a.shift : cst + CF::C_SHIFT;
@@ -419,8 +430,11 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       dphase ^= 1;
       ptx::tc_fence_after();
     };
-    // GLU block epilogue: D -> g (+ residual), prev updated; bias from consts.
-    // u = D + b; out = u_lin * sigmoid(u_gate) [; out = (out + prev) * sqrt(.5)]
+    // GLU block epilogue on the accumulator, 8 columns (4 pairs) at a time.
+    // Host-folded constants (tc_pack): gate columns carry -log2(e), residual
+    // blocks' linear columns carry sqrt(.5); b = [b_lin' (H) | -log2e*b_gate (H)].
+    //   e = 2^(gate'+nb) = exp(-u_gate);  sigma = 1/(1+e)  (one rcp per pair:
+    //   q = 1/(d0 d1), sigma0 = d1 q, sigma1 = d0 q);  out = (lin'+b')*sigma [+ sqrt(.5)*prev]
     auto glu = [&](const float* b, bool residual, float (&prev)[H]) {
 #pragma unroll
       for (int j0 = 0; j0 < H; j0 += 8) {
@@ -429,13 +443,61 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         tmem_load_n<8>(tD + H + j0, gate);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float ug = gate[i] + b[H + j0 + i];
-          const float e = ex2_approx(-ug * kLog2e);
-          const float v = (lin[i] + b[j0 + i]) * rcp_approx(1.0f + e);
-          prev[j0 + i] = residual ? (v + prev[j0 + i]) * kR : v;
+        for (int i = 0; i < 8; i += 2) {
+          const float2 nb = *reinterpret_cast<const float2*>(b + H + j0 + i);
+          const float2 bl = *reinterpret_cast<const float2*>(b + j0 + i);
+          float2 arg = __fadd2_rn(f2(gate[i], gate[i + 1]), nb);
+          arg.x = fminf(arg.x, 63.0f);       // keep d0*d1 finite (sigma < 2^-63 there)
+          arg.y = fminf(arg.y, 63.0f);
+          const float2 d = __fadd2_rn(f2(ex2_approx(arg.x), ex2_approx(arg.y)), f2(1.0f, 1.0f));
+          const float q = rcp_approx(d.x * d.y);
+          const float2 sg = __fmul2_rn(f2(d.y, d.x), f2(q, q));
+          const float2 l = __fadd2_rn(f2(lin[i], lin[i + 1]), bl);
+          float2 o;
+          if (residual) {
+            const float2 rp = __fmul2_rn(f2(prev[j0 + i], prev[j0 + i + 1]), f2(kR, kR));
+            o = __ffma2_rn(l, sg, rp);
+          } else {
+            o = __fmul2_rn(l, sg);
+          }
+          prev[j0 + i] = o.x;
+          prev[j0 + i + 1] = o.y;
         }
       }
+    };
+    // Row outputs staged in `ts` go to global: dense mode = one TMA bulk store
+    // (+ a coalesced tail), transpose mode = cooperative coalesced stores.
+    auto flush_rows = [&](float* dst, int nrows) {
+      if constexpr (CF::DENSE_IO) {
+        ptx::fence_async_shared();
+        ptx::named_bar_sync(bar_id, 128);
+        const int ne = nrows * F;
+        const bool al = ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+        const int nb = al ? ((ne * 4) & ~15) / 4 : 0;
+        if (leader && nb > 0) {
+          ptx::bulk_s2g(dst, ts, (uint32_t)nb * 4u);
+          ptx::bulk_commit();
+        }
+        for (int e = nb + t; e < ne; e += 128) dst[e] = ts[e];
+      } else {
+        ptx::named_bar_sync(bar_id, 128);
+        for (int e = t; e < nrows * F; e += 128) {
+          const int rr = e / F, ff = e - rr * F;
+          dst[e] = ts[ff * 129 + rr];
+        }
+      }
+    };
+    // ts is about to be rewritten: the previous bulk store must have read it
+    // and every thread must be done with its previous contents.
+    auto claim_ts = [&]() {
+      if constexpr (CF::DENSE_IO) {
+        if (leader) ptx::bulk_wait_read0();
+      }
+      ptx::named_bar_sync(bar_id, 128);
+    };
+    auto ts_at = [&](int f) -> float& {
+      if constexpr (CF::DENSE_IO) return ts[t * F + f];
+      else return ts[f * 129 + t];
     };
 
     for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
@@ -446,13 +508,21 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       const bool valid = t < nrows;
       const int64_t row = r0 + t;
 
-      // ---- x tile: staging (TMA) -> [F][129] transpose -> per-row normalize ----
+      // ---- x tile (TMA-staged) -> this thread's row ----
       ptx::mbar_wait(&bars->xfull[g], xphase);
       xphase ^= 1;
-      {
-        const int ne = nrows * F;
-        const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
-        ptx::named_bar_sync(bar_id, 128);   // previous tile's readers of ts are done
+      const int ne = nrows * F;
+      const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
+      float xr[F];
+      if constexpr (CF::DENSE_IO) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          const int e = t * F + f;
+          xr[f] = (e < nbulk) ? xs[e] : (e < ne ? __ldg(a.x + r0 * F + e) : 0.0f);
+        }
+        ptx::mbar_arrive(&bars->xempty[g]);   // staging buffer may be refilled
+      } else {
+        claim_ts();
         for (int e = t; e < 128 * F; e += 128) {
           float v = 0.0f;
           if (e < nbulk) v = xs[e];
@@ -461,7 +531,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           ts[ff * 129 + rr] = v;
         }
         ptx::named_bar_sync(bar_id, 128);
-        ptx::mbar_arrive(&bars->xempty[g]);  // staging buffer may be refilled
+        ptx::mbar_arrive(&bars->xempty[g]);
+#pragma unroll
+        for (int f = 0; f < F; ++f) xr[f] = ts[f * 129 + t];
       }
       // xn = (x - mean) * rsqrt(var + eps) (network.py:118-120); prior = 1; agg = 0
       {
@@ -475,9 +547,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
             one[i] = 1.0f;
             zero[i] = 0.0f;
             if (f < F) {
-              const float xv = ts[f * 129 + t];
-              bad |= !isfinite(xv);
-              xn[i] = a.normalized ? xv : (xv - shift[f]) * scale[f];
+              bad |= !isfinite(xr[f]);
+              xn[i] = a.normalized ? xr[f] : (xr[f] - shift[f]) * scale[f];
             } else {
               xn[i] = 0.0f;
             }
@@ -546,19 +617,29 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         });
 #pragma unroll
         for (int f = 0; f < F; ++f) z[f] -= zmax;                     // sparsemax.py:32
+        // tau: Michelot fixed point from tau0 = -1 (support = {z > tau}); its
+        // support equals the reference's sort/cumsum/count k (sparsemax.py:33-39).
         float tau = -1.0f;
-        int cnt_prev = F + 1;
-        for (int it = 0; it <= F; ++it) {                             // sort-free support search
-          float sm = 0.0f;
-          int c = 0;
+        float cnt_prev = (float)(F + 1);
+        for (int it = 0; it <= F; ++it) {
+          float s0 = 0.0f, s1 = 0.0f, c0 = 0.0f, c1 = 0.0f;
 #pragma unroll
-          for (int f = 0; f < F; ++f)
-            if (z[f] > tau) { sm += z[f]; ++c; }
+          for (int f = 0; f < F; f += 2) {
+            const float m0 = z[f] > tau ? 1.0f : 0.0f;
+            s0 = fmaf(m0, z[f], s0);
+            c0 += m0;
+            if (f + 1 < F) {
+              const float m1 = z[f + 1] > tau ? 1.0f : 0.0f;
+              s1 = fmaf(m1, z[f + 1], s1);
+              c1 += m1;
+            }
+          }
+          const float c = c0 + c1;
           if (c >= cnt_prev) break;
           cnt_prev = c;
-          tau = __fdiv_rn(sm - 1.0f, (float)c);                       // sparsemax.py:39
+          tau = __fdiv_rn((s0 + s1) - 1.0f, c);                      // sparsemax.py:39
         }
-        ptx::named_bar_sync(bar_id, 128);    // previous readers of ts are done
+        claim_ts();
         chunked<CF::K1>([&](auto o, auto l) {
           constexpr int O = decltype(o)::value, L = decltype(l)::value;
           constexpr int LF = (O + L <= F) ? L : (O < F ? F - O : 0);
@@ -575,7 +656,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
               const float m = fmaxf(z[f] - tau, 0.0f);                // sparsemax.py:40
               pr[i] = pr[i] * (p.gamma - m);                          // network.py:237
               xm[i] = m * xnv[i];                                     // network.py:238
-              ts[f * 129 + t] = m;
+              ts_at(f) = m;
             } else {
               xm[i] = 0.0f;
             }
@@ -584,15 +665,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           store_a<CF, L>(tA + O, tAL + O, xm);
         });
         arrive_a();
-        ptx::named_bar_sync(bar_id, 128);
-        // masks[s-1] tile: coalesced store from the [F][129] buffer (network.py:246)
-        if (a.masks) {
-          float* dst = a.masks + ((int64_t)(s - 1) * a.rows + r0) * F;
-          for (int e = t; e < nrows * F; e += 128) {
-            const int rr = e / F, ff = e - rr * F;
-            dst[e] = ts[ff * 129 + rr];
-          }
-        }
+        // masks[s-1] tile (network.py:246)
+        if (a.masks) flush_rows(a.masks + ((int64_t)(s - 1) * a.rows + r0) * F, nrows);
+        else ptx::named_bar_sync(bar_id, 128);
         transform(s);
         // d = relu(f[:, :n_d]); d_sum += d; eta = sum(d); agg += eta*m (network.py:241-245)
         float eta = 0.0f;
@@ -614,10 +689,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           tmem_load_n<L>(tAG + O, ag);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < L; ++i) {
-            const float base = reset ? 0.0f : ag[i];
-            ag[i] = fmaf(w, ts[(O + i) * 129 + t], base);
-          }
+          for (int i = 0; i < L; ++i) ag[i] = fmaf(w, ts_at(O + i), reset ? 0.0f : ag[i]);
           tmem_store_n<L>(tAG + O, ag);
         });
       }
@@ -651,34 +723,21 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       }
       // ---- importance = agg / sum(agg), or mean_s(masks) (network.py:258-261) ----
       {
+        float ag[F];
+        tmem_load_n<F>(tAG, ag);
+        ptx::tmem_ld_wait();
         float tot = 0.0f;
-        chunked<F>([&](auto o, auto l) {
-          constexpr int O = decltype(o)::value, L = decltype(l)::value;
-          float ag[L];
-          tmem_load_n<L>(tAG + O, ag);
-          ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < L; ++i) tot += ag[i];
-        });
-        ptx::named_bar_sync(bar_id, 128);     // mask readers of ts are done
+        for (int f = 0; f < F; ++f) tot += ag[f];
         const float div = all_eta_zero ? (float)S : tot;
-        chunked<F>([&](auto o, auto l) {
-          constexpr int O = decltype(o)::value, L = decltype(l)::value;
-          float ag[L];
-          tmem_load_n<L>(tAG + O, ag);
-          ptx::tmem_ld_wait();
+        claim_ts();
 #pragma unroll
-          for (int i = 0; i < L; ++i) ts[(O + i) * 129 + t] = ag[i] / div;
-        });
-        ptx::named_bar_sync(bar_id, 128);
-        if (a.importance) {
-          float* dst = a.importance + r0 * F;
-          for (int e = t; e < nrows * F; e += 128) {
-            const int rr = e / F, ff = e - rr * F;
-            dst[e] = ts[ff * 129 + rr];
-          }
-        }
+        for (int f = 0; f < F; ++f) ts_at(f) = ag[f] / div;
+        if (a.importance) flush_rows(a.importance + r0 * F, nrows);
       }
+    }
+    if constexpr (CF::DENSE_IO) {
+      if (leader) ptx::bulk_wait0();
     }
   }
 

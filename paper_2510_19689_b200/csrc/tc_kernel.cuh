@@ -436,14 +436,15 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     //   e = 2^(gate'+nb) = exp(-u_gate);  sigma = 1/(1+e)  (one rcp per pair:
     //   q = 1/(d0 d1), sigma0 = d1 q, sigma1 = d0 q);  out = (lin'+b')*sigma [+ sqrt(.5)*prev]
     auto glu = [&](const float* b, bool residual, float (&prev)[H]) {
+      constexpr int CW = H < 32 ? H : 32;      // columns per TMEM wait (ILP across CW/2 pairs)
 #pragma unroll
-      for (int j0 = 0; j0 < H; j0 += 8) {
-        float lin[8], gate[8];
-        tmem_load_n<8>(tD + j0, lin);
-        tmem_load_n<8>(tD + H + j0, gate);
+      for (int j0 = 0; j0 < H; j0 += CW) {
+        float lin[CW], gate[CW];
+        tmem_load_n<CW>(tD + j0, lin);
+        tmem_load_n<CW>(tD + H + j0, gate);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 8; i += 2) {
+        for (int i = 0; i < CW; i += 2) {
           const float2 nb = *reinterpret_cast<const float2*>(b + H + j0 + i);
           const float2 bl = *reinterpret_cast<const float2*>(b + j0 + i);
           float2 arg = __fadd2_rn(f2(gate[i], gate[i + 1]), nb);
@@ -617,27 +618,38 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         });
 #pragma unroll
         for (int f = 0; f < F; ++f) z[f] -= zmax;                     // sparsemax.py:32
-        // tau: Michelot fixed point from tau0 = -1 (support = {z > tau}); its
-        // support equals the reference's sort/cumsum/count k (sparsemax.py:33-39).
-        float tau = -1.0f;
+        // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
+        // monotone from any lower bound of tau*; its support equals the
+        // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
+        // max(-1, (sum z - 1)/F): both bound tau* from below (the max element
+        // alone; all elements in the support).
+        float tau;
+        {
+          float2 acc = f2(0.0f, 0.0f);
+#pragma unroll
+          for (int f = 0; f + 1 < F; f += 2) acc = __fadd2_rn(acc, f2(z[f], z[f + 1]));
+          float tot = acc.x + acc.y;
+          if constexpr (F % 2) tot += z[F - 1];
+          tau = fmaxf(-1.0f, (tot - 1.0f) * (1.0f / (float)F));
+        }
         float cnt_prev = (float)(F + 1);
         for (int it = 0; it <= F; ++it) {
-          float s0 = 0.0f, s1 = 0.0f, c0 = 0.0f, c1 = 0.0f;
+          float2 sm2 = f2(0.0f, 0.0f), c2 = f2(0.0f, 0.0f);
 #pragma unroll
-          for (int f = 0; f < F; f += 2) {
-            const float m0 = z[f] > tau ? 1.0f : 0.0f;
-            s0 = fmaf(m0, z[f], s0);
-            c0 += m0;
-            if (f + 1 < F) {
-              const float m1 = z[f + 1] > tau ? 1.0f : 0.0f;
-              s1 = fmaf(m1, z[f + 1], s1);
-              c1 += m1;
-            }
+          for (int f = 0; f + 1 < F; f += 2) {
+            const float2 m = f2(z[f] > tau ? 1.0f : 0.0f, z[f + 1] > tau ? 1.0f : 0.0f);
+            sm2 = __ffma2_rn(m, f2(z[f], z[f + 1]), sm2);
+            c2 = __fadd2_rn(c2, m);
           }
-          const float c = c0 + c1;
+          float sm = sm2.x + sm2.y, c = c2.x + c2.y;
+          if constexpr (F % 2) {
+            const float m = z[F - 1] > tau ? 1.0f : 0.0f;
+            sm = fmaf(m, z[F - 1], sm);
+            c += m;
+          }
           if (c >= cnt_prev) break;
           cnt_prev = c;
-          tau = __fdiv_rn((s0 + s1) - 1.0f, c);                      // sparsemax.py:39
+          tau = __fdiv_rn(sm - 1.0f, c);                              // sparsemax.py:39
         }
         claim_ts();
         chunked<CF::K1>([&](auto o, auto l) {

@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -268,12 +269,30 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
     a.shift = ss + m->cfg.feature_count;
     TBN_CUDA(tbn::launch_batch_stats(x, rows, m->cfg.feature_count, ss, ss + m->cfg.feature_count, s));
   }
+  // Development aid: TBN_TRACE=1 records a clock64 timeline of CTA 0 and
+  // prints it to stderr after a synchronizing copy (never set in production).
+  static const bool trace_on = getenv("TBN_TRACE") != nullptr;
+  static unsigned long long* d_trace = nullptr;
+  if (trace_on && m->precision != TBN_PREC_FP32) {
+    if (!d_trace) cudaMalloc(&d_trace, 4096 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_trace, 0, 4096 * sizeof(unsigned long long), s);
+    a.trace = d_trace;
+  }
   cudaError_t e;
   if (m->precision == TBN_PREC_FP32)
     e = tbn::launch_simt(m->simt, a, m->num_sms, s);
   else
     e = tbn::launch_tc(m->tc, a, m->num_sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
+  if (a.trace) {
+    std::vector<unsigned long long> h(4096);
+    cudaMemcpyAsync(h.data(), d_trace, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const unsigned long long t0 = h[0];
+    fprintf(stderr, "TRACE rows=%lld\n", (long long)rows);
+    for (int k = 0; k < 4096; ++k)
+      if (h[k]) fprintf(stderr, "TRACE %d %lld\n", k, (long long)(h[k] - t0));
+  }
   return TBN_OK;
 }
 

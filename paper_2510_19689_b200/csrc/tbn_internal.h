@@ -32,6 +32,7 @@ struct ForwardArgs {
   float* importance;
   int32_t* pred;
   int32_t* err_flag;
+  unsigned long long* trace;   // debug timeline (TBN_TRACE env); null in production
 };
 
 size_t simt_smem_bytes(const SimtParams& p);

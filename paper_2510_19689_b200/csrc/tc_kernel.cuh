@@ -276,6 +276,12 @@ __device__ __forceinline__ bool is_resident(int kind) {
 }
 
 // ---------------------------------------------------------------------------
+// Debug timeline: slot k of CTA 0 <- clock64 (only when a.trace is set).
+#define TBN_TRACE(k)                                                       \
+  do {                                                                     \
+    if (a.trace && blockIdx.x == 0 && (k) < 4096) a.trace[(k)] = clock64(); \
+  } while (0)
+
 template <class CF>
 __global__ void __launch_bounds__(CF::THREADS, 1)
 tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
@@ -301,11 +307,13 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     ptx::mbar_init(&bars->cfull, 1);
     ptx::fence_mbar_init();
   }
+  if (threadIdx.x == 0) TBN_TRACE(0);
   if (warp == 0) ptx::tmem_alloc<CF::TCOLS>(&bars->tmem_base);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
+  if (threadIdx.x == 0) TBN_TRACE(1);
 
   const int producer_warp = NG * 4 + 1, mma_warp = NG * 4;
 
@@ -375,6 +383,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
             ptx::mbar_wait(&bars->wfull[slot], wphase);
             bsm = ptx::smem_u32(smem + SM::OFF_RING + slot * CF::SLOT);
           }
+          if (pair == blockIdx.x) TBN_TRACE(2000 + j);
           const int K = kind == 0 ? CF::K1 : (kind == 4 ? NA : H);
           const int N = kind == 4 ? CF::FN : CF::N2;
           const uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtTF32, 128, N);
@@ -385,6 +394,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
             ptx::mbar_wait(&bars->afull[g], aphase[g]);
             aphase[g] ^= 1;
             ptx::tc_fence_after();
+            if (pair == blockIdx.x) TBN_TRACE(1000 + (j * NG + g) * 2);
             const uint32_t tg = tbase + (uint32_t)(g * CF::TCOLS_G);
             for (int k0 = 0; k0 < K; k0 += 8) {
               const uint64_t bd = ptx::smem_desc(bsm + (uint32_t)k0 * 32u, 128u, sbo);
@@ -396,6 +406,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
               }
             }
             ptx::mma_commit(&bars->dfull[g]);
+            if (pair == blockIdx.x) TBN_TRACE(1001 + (j * NG + g) * 2);
           }
           if (!res) {
             ptx::mma_commit(&bars->wempty[slot]);
@@ -420,15 +431,18 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     const float* shift = a.shift ? a.shift : cst + CF::C_SHIFT;
     uint32_t xphase = 0, dphase = 0;
 
+    int tr_a = 0, tr_d = 0;
     auto arrive_a = [&]() {
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
+      if (t == 0) { TBN_TRACE(3000 + 2 * g * 200 + tr_a); ++tr_a; }
       ptx::mbar_arrive(&bars->afull[g]);
     };
     auto wait_d = [&]() {
       ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
       ptx::tc_fence_after();
+      if (t == 0) { TBN_TRACE(3200 + 2 * g * 200 + tr_d); ++tr_d; }
     };
     // GLU block epilogue on the accumulator, 8 columns (4 pairs) at a time.
     // Host-folded constants (tc_pack): gate columns carry -log2(e), residual
@@ -510,7 +524,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       const int64_t row = r0 + t;
 
       // ---- x tile (TMA-staged) -> this thread's row ----
+      if (t == 0) TBN_TRACE(10 + g);
       ptx::mbar_wait(&bars->xfull[g], xphase);
+      if (t == 0) TBN_TRACE(12 + g);
       xphase ^= 1;
       const int ne = nrows * F;
       const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
@@ -755,6 +771,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TBN_TRACE(2);
   if (warp == 0) ptx::tmem_dealloc<CF::TCOLS>(tbase);
 }
 

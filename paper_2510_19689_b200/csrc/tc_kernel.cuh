@@ -1,19 +1,25 @@
 // tc_kernel.cuh — K1: the whole TabNet forward (network.py:195-267) as ONE
-// persistent sm_100a kernel.  Row tiles of 128 (one row per epilogue thread,
-// one TMEM lane per row) stay on-chip for all decision steps:
+// persistent sm_100a kernel.  Row tiles of 128 (one TMEM lane per row) stay
+// on-chip for all decision steps:
 //
 //   TMEM (per row-group of 128 rows)      SMEM (per CTA)
-//   [D  accumulator, DW cols ]            consts: affine, biases, head
+//   [D  accumulator, DW cols ]            consts: affine, folded biases, head
 //   [A  operand hi,  KA cols ]            resident shared1/shared2 (if they fit)
 //   [A  operand lo,  KA cols ] (3xTF32)   weight ring (per-step B operands, TMA bulk)
-//   [xn F][prior F][agg F]  per-row state x staging (TMA bulk, 1 tile ahead)
-//                                         [F][129] transpose buffer (coalesced I/O)
+//   [xn F][prior F][agg F]  per-row state x staging (TMA bulk, one tile ahead)
+//                                         row staging for coalesced/bulk output
 //
-// Warp roles: NG row-groups x 4 epilogue warps (thread-per-row GLU / attentive /
-// sparsemax / aggregation math on CUDA cores), 1 MMA warp (a single thread
-// issues tcgen05.mma kind::tf32 with A from TMEM, B from SMEM), 1 producer warp
-// (cp.async.bulk of x tiles and weight blocks).  With NG = 2 the two row-groups
-// ping-pong: one group's epilogue overlaps the other group's MMAs.
+// Warp roles: NG row-groups x 8 warps, nothing else.  Within a
+// group, warps w and w+4 share TMEM lane quarter w%4 (= the same 32 rows) and
+// split each row's columns: "half 0" owns GLU columns [0, H/2) — the decision
+// part d — and "half 1" owns [H/2, H) — the attention state a (n_d == n_a).
+// Sparsemax is computed redundantly by both halves from TMEM; features are
+// split for the prior/mask/A updates.  After every A write the group meets at
+// a 256-thread named barrier and one elected thread issues the tcgen05.mma
+// chain (kind::tf32, A from TMEM, B from SMEM) and commits it to the group's
+// mbarrier — no separate MMA or producer warp, no cross-group lockstep: that
+// thread also streams the group's own weight ring and next x tile (TMA bulk),
+// so the NG groups run independently and overlap each other's MMA / epilogue.
 //
 // Per-row arithmetic is identical for every row whatever the batch size, tile
 // position, grid size or group: the batch-invariance contract (network.py:11-14).
@@ -77,15 +83,23 @@ struct Cfg {
   static constexpr int RING_SLOT_ALL = cmax(cmax(B_SH1, B_HID), B_ATT);
   static constexpr int RING_SLOT_RES = cmax(B_HID, B_ATT);
   static constexpr int SMEM_BUDGET = 225 * 1024;
-  static constexpr bool RESIDENT = FIXED + B_SH1 + B_HID + 3 * RING_SLOT_RES <= SMEM_BUDGET;
+  // Each row group streams its own weight ring (NSLOT slots); shared1/shared2
+  // stay resident for the whole CTA when they fit.
+  static constexpr bool RESIDENT = FIXED + B_SH1 + B_HID + NG * 2 * RING_SLOT_RES <= SMEM_BUDGET;
   static constexpr int SLOT = RESIDENT ? RING_SLOT_RES : RING_SLOT_ALL;
-  static constexpr int NSLOT = RESIDENT ? 3 : ((FIXED + 3 * SLOT <= SMEM_BUDGET) ? 3 : 2);
   static constexpr int RES_BYTES = RESIDENT ? (B_SH1 + B_HID) : 0;
-  static constexpr int SMEM_BYTES = FIXED + RES_BYTES + NSLOT * SLOT;
+  static constexpr int NSLOT = (FIXED + RES_BYTES + NG * 3 * SLOT <= SMEM_BUDGET) ? 3 : 2;
+  static constexpr int SMEM_BYTES = FIXED + RES_BYTES + NG * NSLOT * SLOT;
+  // non-resident blocks per tile (the ring sequence)
+  static constexpr int NB = RESIDENT ? 2 + 3 * S : 4 + 5 * S;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared-memory plan exceeds 227 KB");
   // GEMMs per tile: step 0 transform (4) + S x (att + transform 4)
   static constexpr int GEMMS = 4 + 5 * S;
-  static constexpr int THREADS = NG * 128 + 64;
+  static constexpr int HH = H / 2;                      // GLU columns per half
+  static constexpr int KH = K1 / 2;                     // shared1 K columns per half
+  static_assert(ND == NA, "column split assumes n_d == n_a (all BASELINE configs)");
+  static_assert(K1 % 8 == 0 && HH % 4 == 0, "half split granularity");
+  static constexpr int THREADS = NG * 256;
 };
 
 // Global-memory weight image (built by the host packer, tc_pack):
@@ -228,17 +242,14 @@ struct Smem {
   static constexpr int OFF_T = OFF_X + CF::NG * CF::XSTAGE;
   static constexpr int OFF_RES = rup(OFF_T + CF::NG * CF::TSTAGE, 1024);
   static constexpr int OFF_RING = OFF_RES + CF::RES_BYTES;
-  static constexpr int OFF_BAR = OFF_RING + CF::NSLOT * CF::SLOT;
+  static constexpr int OFF_BAR = OFF_RING + CF::NG * CF::NSLOT * CF::SLOT;
   static constexpr int TOTAL = OFF_BAR + 256;
   static_assert(TOTAL <= 227 * 1024, "smem");
 };
 
 struct Bars {
-  uint64_t wfull[4];
-  uint64_t wempty[4];
+  uint64_t wfull[2][4];    // per row group ring
   uint64_t xfull[2];
-  uint64_t xempty[2];
-  uint64_t afull[2];
   uint64_t dfull[2];
   uint64_t cfull;
   uint32_t tmem_base;
@@ -254,6 +265,20 @@ __device__ __forceinline__ void gemm_of(int j, int& kind, int& step) {
   step = q / 5 + 1;
   int r = q % 5;
   kind = (r == 0) ? 4 : r - 1;
+}
+
+// Position u (0..NB-1) of a tile's ring sequence -> (kind, step).
+template <class CF>
+__device__ __forceinline__ void ring_block(int u, int& kind, int& step) {
+  if constexpr (CF::RESIDENT) {
+    if (u < 2) { kind = 2 + u; step = 0; return; }
+    const int q = u - 2;
+    step = q / 3 + 1;
+    const int r = q % 3;
+    kind = (r == 0) ? 4 : r + 1;
+  } else {
+    gemm_of(u, kind, step);
+  }
 }
 
 template <class CF>
@@ -277,8 +302,8 @@ __device__ __forceinline__ bool is_resident(int kind) {
 
 // ---------------------------------------------------------------------------
 // Debug timeline: slot k of CTA 0 <- clock64 (only when a.trace is set).
-#define TBN_TRACE(k)                                                       \
-  do {                                                                     \
+#define TBN_TRACE(k)                                                        \
+  do {                                                                      \
     if (a.trace && blockIdx.x == 0 && (k) < 4096) a.trace[(k)] = clock64(); \
   } while (0)
 
@@ -288,6 +313,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   using SM = Smem<CF>;
   constexpr int F = CF::F, H = CF::H, ND = CF::ND, NA = CF::NA, S = CF::S, C = CF::C, NG = CF::NG;
+  constexpr int HH = CF::HH, KH = CF::KH, K1 = CF::K1;
   const float* cst = reinterpret_cast<const float*>(smem + SM::OFF_CONST);
   Bars* bars = reinterpret_cast<Bars*>(smem + SM::OFF_BAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -297,170 +323,141 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
 
   // ---- setup ----
   if (threadIdx.x == 0) {
-    for (int i = 0; i < CF::NSLOT; ++i) { ptx::mbar_init(&bars->wfull[i], 1); ptx::mbar_init(&bars->wempty[i], 1); }
+    TBN_TRACE(0);
     for (int g = 0; g < NG; ++g) {
+      for (int i = 0; i < CF::NSLOT; ++i) ptx::mbar_init(&bars->wfull[g][i], 1);
       ptx::mbar_init(&bars->xfull[g], 1);
-      ptx::mbar_init(&bars->xempty[g], 128);
-      ptx::mbar_init(&bars->afull[g], 128);
       ptx::mbar_init(&bars->dfull[g], 1);
     }
     ptx::mbar_init(&bars->cfull, 1);
     ptx::fence_mbar_init();
+    ptx::mbar_arrive_expect_tx(&bars->cfull, CF::CONST_BYTES + CF::RES_BYTES);
+    ptx::bulk_g2s(smem + SM::OFF_CONST, p.wimg, CF::CONST_BYTES, &bars->cfull);
+    if constexpr (CF::RESIDENT) {
+      ptx::bulk_g2s(smem + SM::OFF_RES, p.wimg + p.off_sh1, CF::B_SH1, &bars->cfull);
+      ptx::bulk_g2s(smem + SM::OFF_RES + CF::B_SH1, p.wimg + p.off_sh2, CF::B_HID, &bars->cfull);
+    }
   }
-  if (threadIdx.x == 0) TBN_TRACE(0);
   if (warp == 0) ptx::tmem_alloc<CF::TCOLS>(&bars->tmem_base);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = bars->tmem_base;
-  if (threadIdx.x == 0) TBN_TRACE(1);
 
-  const int producer_warp = NG * 4 + 1, mma_warp = NG * 4;
-
-  if (warp == producer_warp) {
-    // ======================= PRODUCER (TMA bulk copies) =======================
-    if (ptx::elect_one()) {
-      uint32_t cbytes = CF::CONST_BYTES + CF::RES_BYTES;
-      ptx::mbar_arrive_expect_tx(&bars->cfull, cbytes);
-      ptx::bulk_g2s(smem + SM::OFF_CONST, p.wimg, CF::CONST_BYTES, &bars->cfull);
-      if constexpr (CF::RESIDENT) {
-        ptx::bulk_g2s(smem + SM::OFF_RES, p.wimg + p.off_sh1, CF::B_SH1, &bars->cfull);
-        ptx::bulk_g2s(smem + SM::OFF_RES + CF::B_SH1, p.wimg + p.off_sh2, CF::B_HID, &bars->cfull);
-      }
-      uint32_t xphase[2] = {0, 0};
-      auto load_x = [&](int64_t pair) {
-        for (int g = 0; g < NG; ++g) {
-          int64_t tile = pair * NG + g;
-          if (tile >= ntiles) continue;
-          ptx::mbar_wait(&bars->xempty[g], xphase[g] ^ 1);
-          xphase[g] ^= 1;
-          int64_t r0 = tile * 128;
-          int64_t nr = a.rows - r0 < 128 ? a.rows - r0 : 128;
-          uint32_t bytes = x_bulk_ok ? (uint32_t)((nr * F * 4) & ~15ll) : 0u;
-          if (bytes) {
-            ptx::mbar_arrive_expect_tx(&bars->xfull[g], bytes);
-            ptx::bulk_g2s(smem + SM::OFF_X + g * CF::XSTAGE, a.x + r0 * F, bytes, &bars->xfull[g]);
-          } else {
-            ptx::mbar_arrive(&bars->xfull[g]);
-          }
-        }
-      };
-      int slot = 0;
-      uint32_t wphase = 0;
-      int64_t pair = blockIdx.x;
-      if (pair < npairs) load_x(pair);
-      for (; pair < npairs; pair += gridDim.x) {
-        for (int j = 0; j < CF::GEMMS; ++j) {
-          int kind, step;
-          gemm_of(j, kind, step);
-          if (j == 2 && pair + gridDim.x < npairs) load_x(pair + gridDim.x);   // prefetch next tiles
-          if (is_resident<CF>(kind)) continue;
-          ptx::mbar_wait(&bars->wempty[slot], wphase ^ 1);
-          uint32_t bytes = block_bytes<CF>(kind);
-          ptx::mbar_arrive_expect_tx(&bars->wfull[slot], bytes);
-          ptx::bulk_g2s(smem + SM::OFF_RING + slot * CF::SLOT, p.wimg + block_offset<CF>(p, kind, step),
-                        bytes, &bars->wfull[slot]);
-          if (++slot == CF::NSLOT) { slot = 0; wphase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == mma_warp) {
-    // ======================= MMA ISSUER (one thread) ===========================
-    if (ptx::elect_one()) {
-      ptx::mbar_wait(&bars->cfull, 0);
-      uint32_t aphase[2] = {0, 0};
-      int slot = 0;
-      uint32_t wphase = 0;
-      for (int64_t pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
-        for (int j = 0; j < CF::GEMMS; ++j) {
-          int kind, step;
-          gemm_of(j, kind, step);
-          const bool res = is_resident<CF>(kind);
-          uint32_t bsm;
-          if (res) {
-            bsm = ptx::smem_u32(smem + SM::OFF_RES + (kind == 0 ? 0 : CF::B_SH1));
-          } else {
-            ptx::mbar_wait(&bars->wfull[slot], wphase);
-            bsm = ptx::smem_u32(smem + SM::OFF_RING + slot * CF::SLOT);
-          }
-          if (pair == blockIdx.x) TBN_TRACE(2000 + j);
-          const int K = kind == 0 ? CF::K1 : (kind == 4 ? NA : H);
-          const int N = kind == 4 ? CF::FN : CF::N2;
-          const uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtTF32, 128, N);
-          const uint32_t sbo = (uint32_t)(K / 4) * 128u;
-          const uint32_t lo_off = (uint32_t)(N * K * 4);
-          for (int g = 0; g < NG; ++g) {
-            if (pair * NG + g >= ntiles) continue;
-            ptx::mbar_wait(&bars->afull[g], aphase[g]);
-            aphase[g] ^= 1;
-            ptx::tc_fence_after();
-            if (pair == blockIdx.x) TBN_TRACE(1000 + (j * NG + g) * 2);
-            const uint32_t tg = tbase + (uint32_t)(g * CF::TCOLS_G);
-            for (int k0 = 0; k0 < K; k0 += 8) {
-              const uint64_t bd = ptx::smem_desc(bsm + (uint32_t)k0 * 32u, 128u, sbo);
-              ptx::mma_tf32_ts(tg + CF::T_D, tg + CF::T_A + k0, bd, idesc, k0 > 0 ? 1u : 0u);
-              if constexpr (CF::X3) {
-                const uint64_t bdl = ptx::smem_desc(bsm + lo_off + (uint32_t)k0 * 32u, 128u, sbo);
-                ptx::mma_tf32_ts(tg + CF::T_D, tg + CF::T_AL + k0, bd, idesc, 1u);
-                ptx::mma_tf32_ts(tg + CF::T_D, tg + CF::T_A + k0, bdl, idesc, 1u);
-              }
-            }
-            ptx::mma_commit(&bars->dfull[g]);
-            if (pair == blockIdx.x) TBN_TRACE(1001 + (j * NG + g) * 2);
-          }
-          if (!res) {
-            ptx::mma_commit(&bars->wempty[slot]);
-            if (++slot == CF::NSLOT) { slot = 0; wphase ^= 1; }
-          }
-        }
-      }
-    }
-  } else {
-    // ======================= EPILOGUE / ROW MATH (thread = row) =================
-    const int g = warp >> 2;                 // row group
-    const int t = threadIdx.x & 127;         // row within tile == TMEM lane
+  {
+    // ======================= ROW GROUPS (thread = (row, column half)) ========
+    const int g = warp >> 3;                  // row group
+    const int half = (warp >> 2) & 1;         // 0: d columns, 1: a columns
+    const int t = (warp & 3) * 32 + lane;     // row within tile == TMEM lane
     const uint32_t tg = tbase + (uint32_t)(g * CF::TCOLS_G) + ((uint32_t)((warp & 3) * 32) << 16);
     const uint32_t tD = tg + CF::T_D, tA = tg + CF::T_A, tAL = tg + CF::T_AL;
     const uint32_t tXN = tg + CF::T_XN, tPR = tg + CF::T_PR, tAG = tg + CF::T_AG;
     const float* xs = reinterpret_cast<const float*>(smem + SM::OFF_X + g * CF::XSTAGE);
     float* ts = reinterpret_cast<float*>(smem + SM::OFF_T + g * CF::TSTAGE);
     const uint32_t bar_id = 1 + g;
-    const bool leader = (t == 0);
+    const bool issuer = ((warp & 7) == 0) && lane == 0;    // half 0, quarter 0, lane 0
+    const bool flusher = ((warp & 7) == 4) && lane == 0;   // half 1, quarter 0, lane 0
+    uint8_t* ring = smem + SM::OFF_RING + g * CF::NSLOT * CF::SLOT;
+    // Issuer-only producer duties for this group: its own weight ring (block u
+    // of the group's sequence lives in slot u % NSLOT) and its next x tile.
+    auto issue_block = [&](uint32_t u) {
+      const int64_t pr = (int64_t)blockIdx.x + (int64_t)(u / CF::NB) * gridDim.x;
+      if (pr >= npairs || pr * NG + g >= ntiles) return;
+      int kind, step;
+      ring_block<CF>((int)(u % CF::NB), kind, step);
+      const uint32_t bytes = block_bytes<CF>(kind);
+      const int sl = (int)(u % CF::NSLOT);
+      ptx::mbar_arrive_expect_tx(&bars->wfull[g][sl], bytes);
+      ptx::bulk_g2s(ring + sl * CF::SLOT, p.wimg + block_offset<CF>(p, kind, step), bytes,
+                    &bars->wfull[g][sl]);
+    };
+    auto issue_x = [&](int64_t pr) {
+      if (pr >= npairs || pr * NG + g >= ntiles) return;
+      const int64_t r0 = (pr * NG + g) * 128;
+      const int64_t nr = a.rows - r0 < 128 ? a.rows - r0 : 128;
+      const uint32_t bytes = x_bulk_ok ? (uint32_t)((nr * F * 4) & ~15ll) : 0u;
+      if (bytes) {
+        ptx::mbar_arrive_expect_tx(&bars->xfull[g], bytes);
+        ptx::bulk_g2s(smem + SM::OFF_X + g * CF::XSTAGE, a.x + r0 * F, bytes, &bars->xfull[g]);
+      } else {
+        ptx::mbar_arrive(&bars->xfull[g]);
+      }
+    };
+    uint32_t ring_used = 0;                   // issuer-only: ring blocks consumed
+    if (issuer) {
+      issue_x(blockIdx.x);
+      for (uint32_t u = 0; u < (uint32_t)CF::NSLOT; ++u) issue_block(u);
+    }
     ptx::mbar_wait(&bars->cfull, 0);
     const float* scale = a.scale ? a.scale : cst + CF::C_SCALE;
     const float* shift = a.shift ? a.shift : cst + CF::C_SHIFT;
     uint32_t xphase = 0, dphase = 0;
 
-    int tr_a = 0, tr_d = 0;
-    auto arrive_a = [&]() {
+    // A is written (both halves) -> barrier -> one thread issues GEMM j of the
+    // tile's sequence -> everyone waits for the accumulator.  `post` runs
+    // between the barrier and the wait (overlaps the MMA).
+    auto gemm = [&](int j, int64_t pair, auto&& post) {
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
-      if (t == 0) { TBN_TRACE(3000 + 2 * g * 200 + tr_a); ++tr_a; }
-      ptx::mbar_arrive(&bars->afull[g]);
-    };
-    auto wait_d = [&]() {
+      ptx::named_bar_sync(bar_id, 256);
+      if (issuer) {
+        ptx::tc_fence_after();
+        int kind, step;
+        gemm_of(j, kind, step);
+        const bool res = is_resident<CF>(kind);
+        uint32_t bsm;
+        if (j == 0) issue_x(pair + gridDim.x);   // every thread has read this tile's x
+        if (res) {
+          bsm = ptx::smem_u32(smem + SM::OFF_RES + (kind == 0 ? 0 : CF::B_SH1));
+        } else {
+          const uint32_t u = ring_used++;
+          ptx::mbar_wait(&bars->wfull[g][u % CF::NSLOT], (u / CF::NSLOT) & 1u);
+          bsm = ptx::smem_u32(ring + (u % CF::NSLOT) * CF::SLOT);
+          // block u-1's MMAs completed (its accumulator was waited on): refill
+          // its slot with block u + NSLOT - 1.
+          if (u >= 1) issue_block(u + CF::NSLOT - 1);
+        }
+        const int K = kind == 0 ? K1 : (kind == 4 ? NA : H);
+        const int N = kind == 4 ? CF::FN : CF::N2;
+        const uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtTF32, 128, N);
+        const uint32_t sbo = (uint32_t)(K / 4) * 128u;
+        const uint32_t lo_off = (uint32_t)(N * K * 4);
+        for (int k0 = 0; k0 < K; k0 += 8) {
+          const uint64_t bd = ptx::smem_desc(bsm + (uint32_t)k0 * 32u, 128u, sbo);
+          ptx::mma_tf32_ts(tD, tA + k0, bd, idesc, k0 > 0 ? 1u : 0u);
+          if constexpr (CF::X3) {
+            const uint64_t bdl = ptx::smem_desc(bsm + lo_off + (uint32_t)k0 * 32u, 128u, sbo);
+            ptx::mma_tf32_ts(tD, tAL + k0, bd, idesc, 1u);
+            ptx::mma_tf32_ts(tD, tA + k0, bdl, idesc, 1u);
+          }
+        }
+        ptx::mma_commit(&bars->dfull[g]);
+      }
+      post();
       ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
       ptx::tc_fence_after();
-      if (t == 0) { TBN_TRACE(3200 + 2 * g * 200 + tr_d); ++tr_d; }
     };
-    // GLU block epilogue on the accumulator, 8 columns (4 pairs) at a time.
+    auto nopost = [] {};
+
+    // GLU epilogue for this half's H/2 output columns (lin | gate blocks of D).
     // Host-folded constants (tc_pack): gate columns carry -log2(e), residual
     // blocks' linear columns carry sqrt(.5); b = [b_lin' (H) | -log2e*b_gate (H)].
     //   e = 2^(gate'+nb) = exp(-u_gate);  sigma = 1/(1+e)  (one rcp per pair:
     //   q = 1/(d0 d1), sigma0 = d1 q, sigma1 = d0 q);  out = (lin'+b')*sigma [+ sqrt(.5)*prev]
-    auto glu = [&](const float* b, bool residual, float (&prev)[H]) {
-      constexpr int CW = H < 32 ? H : 32;      // columns per TMEM wait (ILP across CW/2 pairs)
+    auto glu = [&](const float* b, bool residual, float (&prev)[HH]) {
+      constexpr int CW = HH < 32 ? HH : 32;
+      const int c0 = half * HH;
 #pragma unroll
-      for (int j0 = 0; j0 < H; j0 += CW) {
+      for (int j0 = 0; j0 < HH; j0 += CW) {
         float lin[CW], gate[CW];
-        tmem_load_n<CW>(tD + j0, lin);
-        tmem_load_n<CW>(tD + H + j0, gate);
+        tmem_load_n<CW>(tD + c0 + j0, lin);
+        tmem_load_n<CW>(tD + H + c0 + j0, gate);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < CW; i += 2) {
-          const float2 nb = *reinterpret_cast<const float2*>(b + H + j0 + i);
-          const float2 bl = *reinterpret_cast<const float2*>(b + j0 + i);
+          const float2 nb = *reinterpret_cast<const float2*>(b + H + c0 + j0 + i);
+          const float2 bl = *reinterpret_cast<const float2*>(b + c0 + j0 + i);
           float2 arg = __fadd2_rn(f2(gate[i], gate[i + 1]), nb);
           arg.x = fminf(arg.x, 63.0f);       // keep d0*d1 finite (sigma < 2^-63 there)
           arg.y = fminf(arg.y, 63.0f);
@@ -480,35 +477,33 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         }
       }
     };
-    // Row outputs staged in `ts` go to global: dense mode = one TMA bulk store
-    // (+ a coalesced tail), transpose mode = cooperative coalesced stores.
+    auto store_half = [&](const float (&v)[HH]) {     // A columns [half*H/2, +H/2)
+      store_a_all<CF, HH>(tA + half * HH, tAL + half * HH, v);
+    };
+    // Row staging -> global: dense mode = TMA bulk store (+ coalesced tail),
+    // transpose mode = cooperative coalesced stores.  Call after a group barrier.
     auto flush_rows = [&](float* dst, int nrows) {
       if constexpr (CF::DENSE_IO) {
-        ptx::fence_async_shared();
-        ptx::named_bar_sync(bar_id, 128);
         const int ne = nrows * F;
         const bool al = ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
         const int nb = al ? ((ne * 4) & ~15) / 4 : 0;
-        if (leader && nb > 0) {
+        if (flusher && nb > 0) {
           ptx::bulk_s2g(dst, ts, (uint32_t)nb * 4u);
           ptx::bulk_commit();
         }
-        for (int e = nb + t; e < ne; e += 128) dst[e] = ts[e];
+        for (int e = nb + threadIdx.x % 256; e < ne; e += 256) dst[e] = ts[e];
       } else {
-        ptx::named_bar_sync(bar_id, 128);
-        for (int e = t; e < nrows * F; e += 128) {
+        for (int e = (int)(threadIdx.x % 256); e < nrows * F; e += 256) {
           const int rr = e / F, ff = e - rr * F;
           dst[e] = ts[ff * 129 + rr];
         }
       }
     };
-    // ts is about to be rewritten: the previous bulk store must have read it
-    // and every thread must be done with its previous contents.
-    auto claim_ts = [&]() {
+    auto claim_ts = [&]() {      // previous readers (incl. a bulk store) done with ts
       if constexpr (CF::DENSE_IO) {
-        if (leader) ptx::bulk_wait_read0();
+        if (flusher) ptx::bulk_wait_read0();
       }
-      ptx::named_bar_sync(bar_id, 128);
+      ptx::named_bar_sync(bar_id, 256);
     };
     auto ts_at = [&](int f) -> float& {
       if constexpr (CF::DENSE_IO) return ts[t * F + f];
@@ -522,101 +517,100 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       const int nrows = (int)(a.rows - r0 < 128 ? a.rows - r0 : 128);
       const bool valid = t < nrows;
       const int64_t row = r0 + t;
+      int j = 0;                                 // GEMM index within the tile
 
-      // ---- x tile (TMA-staged) -> this thread's row ----
-      if (t == 0) TBN_TRACE(10 + g);
+      // ---- x tile (TMA-staged): xn = (x - mean) * rsqrt(var + eps) for this
+      // half's features (network.py:118-120); prior = 1; agg = 0 ----
       ptx::mbar_wait(&bars->xfull[g], xphase);
-      if (t == 0) TBN_TRACE(12 + g);
       xphase ^= 1;
-      const int ne = nrows * F;
-      const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
-      float xr[F];
-      if constexpr (CF::DENSE_IO) {
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-          const int e = t * F + f;
-          xr[f] = (e < nbulk) ? xs[e] : (e < ne ? __ldg(a.x + r0 * F + e) : 0.0f);
-        }
-        ptx::mbar_arrive(&bars->xempty[g]);   // staging buffer may be refilled
-      } else {
-        claim_ts();
-        for (int e = t; e < 128 * F; e += 128) {
-          float v = 0.0f;
-          if (e < nbulk) v = xs[e];
-          else if (e < ne) v = a.x[r0 * F + e];
-          const int rr = e / F, ff = e - rr * F;
-          ts[ff * 129 + rr] = v;
-        }
-        ptx::named_bar_sync(bar_id, 128);
-        ptx::mbar_arrive(&bars->xempty[g]);
-#pragma unroll
-        for (int f = 0; f < F; ++f) xr[f] = ts[f * 129 + t];
-      }
-      // xn = (x - mean) * rsqrt(var + eps) (network.py:118-120); prior = 1; agg = 0
       {
+        const int ne = nrows * F;
+        const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
+        if constexpr (!CF::DENSE_IO) {
+          claim_ts();
+          for (int e = (int)(threadIdx.x % 256); e < 128 * F; e += 256) {
+            float v = 0.0f;
+            if (e < nbulk) v = xs[e];
+            else if (e < ne) v = a.x[r0 * F + e];
+            const int rr = e / F, ff = e - rr * F;
+            ts[ff * 129 + rr] = v;
+          }
+          ptx::named_bar_sync(bar_id, 256);
+        }
         int bad = 0;
-        chunked<CF::K1>([&](auto o, auto l) {
-          constexpr int O = decltype(o)::value, L = decltype(l)::value;
-          float xn[L], one[L], zero[L];
+        auto xn_half = [&](auto hc) {
+          constexpr int HB = decltype(hc)::value;
+          chunked<KH>([&](auto o, auto l) {
+            constexpr int O = decltype(o)::value, L = decltype(l)::value;
+            constexpr int FB = HB * KH + O;                          // first feature
+            constexpr int LF = (FB + L <= F) ? L : (FB < F ? F - FB : 0);
+            float xn[L], one[L];
 #pragma unroll
-          for (int i = 0; i < L; ++i) {
-            const int f = O + i;
-            one[i] = 1.0f;
-            zero[i] = 0.0f;
-            if (f < F) {
-              bad |= !isfinite(xr[f]);
-              xn[i] = a.normalized ? xr[f] : (xr[f] - shift[f]) * scale[f];
-            } else {
-              xn[i] = 0.0f;
+            for (int i = 0; i < L; ++i) {
+              const int f = FB + i;
+              one[i] = 1.0f;
+              if (f < F) {
+                float xv;
+                if constexpr (CF::DENSE_IO) {
+                  const int e = t * F + f;
+                  xv = (e < nbulk) ? xs[e] : (e < ne ? __ldg(a.x + r0 * F + e) : 0.0f);
+                } else {
+                  xv = ts[f * 129 + t];
+                }
+                bad |= !isfinite(xv);
+                xn[i] = a.normalized ? xv : (xv - shift[f]) * scale[f];
+              } else {
+                xn[i] = 0.0f;
+              }
             }
-          }
-          constexpr int LF = (O + L <= F) ? L : (O < F ? F - O : 0);
-          if constexpr (LF > 0) {
-            tmem_store_n<LF>(tXN + O, xn);
-            tmem_store_n<LF>(tPR + O, one);
-            tmem_store_n<LF>(tAG + O, zero);
-          }
-          store_a<CF, L>(tA + O, tAL + O, xn);
-        });
-        if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
-        arrive_a();
-      }
-      float prev[H];
-      float dsum[ND];
+            if constexpr (LF > 0) {
+              tmem_store_n<LF>(tXN + FB, xn);
+              tmem_store_n<LF>(tPR + FB, one);
+            }
+            store_a<CF, L>(tA + FB, tAL + FB, xn);
+          });
+        };
+        if (half == 0) {
+          xn_half(std::integral_constant<int, 0>{});
+          chunked<F>([&](auto o, auto l) {                           // agg = 0 (owned by half 0)
+            constexpr int O = decltype(o)::value, L = decltype(l)::value;
+            float zero[L];
 #pragma unroll
-      for (int j = 0; j < ND; ++j) dsum[j] = 0.0f;
+            for (int i = 0; i < L; ++i) zero[i] = 0.0f;
+            tmem_store_n<L>(tAG + O, zero);
+          });
+        } else {
+          xn_half(std::integral_constant<int, 1>{});
+        }
+        if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
+      }
+      float prev[HH];
+      float dsum[HH];                            // half 0: d_sum (n_d == H/2)
+#pragma unroll
+      for (int i = 0; i < HH; ++i) dsum[i] = 0.0f;
       bool all_eta_zero = true;
 
       // feature transformer (network.py:124-141): 4 GEMM+GLU blocks
-      auto transform = [&](int step) {
-        wait_d();
+      auto transform = [&](int step, auto&& post_first) {
+        gemm(j++, pair, post_first);
         glu(cst + CF::C_BSH1, false, prev);                          // g1 = GLU(u1)
-        store_a_all<CF, H>(tA, tAL, prev);
-        arrive_a();
-        wait_d();
+        store_half(prev);
+        gemm(j++, pair, nopost);
         glu(cst + CF::C_BSH2, true, prev);                           // g2
-        store_a_all<CF, H>(tA, tAL, prev);
-        arrive_a();
-        wait_d();
+        store_half(prev);
+        gemm(j++, pair, nopost);
         glu(cst + CF::C_BFC1 + step * CF::N2, true, prev);           // g3
-        store_a_all<CF, H>(tA, tAL, prev);
-        arrive_a();
-        wait_d();
+        store_half(prev);
+        gemm(j++, pair, nopost);
         glu(cst + CF::C_BFC2 + step * CF::N2, true, prev);           // g4 = f
       };
 
-      transform(0);                                                   // network.py:226-227
+      transform(0, nopost);                                           // network.py:226-227
       for (int s = 1; s <= S; ++s) {
-        // A <- a = f[:, n_d:]
-        {
-          float av[NA];
-#pragma unroll
-          for (int k = 0; k < NA; ++k) av[k] = prev[ND + k];
-          store_a_all<CF, NA>(tA, tAL, av);
-          arrive_a();
-        }
+        // A <- a = f[:, n_d:]  (half 1 owns it)
+        if (half == 1) store_a_all<CF, NA>(tA, tAL, prev);
+        gemm(j++, pair, nopost);
         // attentive FC + prior + sparsemax (network.py:233-236, sparsemax.py:13-41)
-        wait_d();
         float z[F];
         const float* batt = cst + CF::C_BATT + (s - 1) * CF::FN;
         float zmax = -INFINITY;
@@ -637,8 +631,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
         // monotone from any lower bound of tau*; its support equals the
         // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
-        // max(-1, (sum z - 1)/F): both bound tau* from below (the max element
-        // alone; all elements in the support).
+        // max(-1, (sum z - 1)/F): both bound tau* from below.
         float tau;
         {
           float2 acc = f2(0.0f, 0.0f);
@@ -668,61 +661,73 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           tau = __fdiv_rn(sm - 1.0f, c);                              // sparsemax.py:39
         }
         claim_ts();
-        chunked<CF::K1>([&](auto o, auto l) {
-          constexpr int O = decltype(o)::value, L = decltype(l)::value;
-          constexpr int LF = (O + L <= F) ? L : (O < F ? F - O : 0);
-          float pr[L], xnv[L], xm[L];
-          if constexpr (LF > 0) {
-            tmem_load_n<LF>(tPR + O, pr);
-            tmem_load_n<LF>(tXN + O, xnv);
-            ptx::tmem_ld_wait();
-          }
-#pragma unroll
-          for (int i = 0; i < L; ++i) {
-            const int f = O + i;
-            if (f < F) {
-              const float m = fmaxf(z[f] - tau, 0.0f);                // sparsemax.py:40
-              pr[i] = pr[i] * (p.gamma - m);                          // network.py:237
-              xm[i] = m * xnv[i];                                     // network.py:238
-              ts_at(f) = m;
-            } else {
-              xm[i] = 0.0f;
+        // this half's features: mask, prior update, xm -> A (network.py:237-238, :246)
+        auto mask_half = [&](auto hc) {
+          constexpr int HB = decltype(hc)::value;
+          chunked<KH>([&](auto o, auto l) {
+            constexpr int O = decltype(o)::value, L = decltype(l)::value;
+            constexpr int FB = HB * KH + O;
+            constexpr int LF = (FB + L <= F) ? L : (FB < F ? F - FB : 0);
+            float pr[L], xnv[L], xm[L];
+            if constexpr (LF > 0) {
+              tmem_load_n<LF>(tPR + FB, pr);
+              tmem_load_n<LF>(tXN + FB, xnv);
+              ptx::tmem_ld_wait();
             }
-          }
-          if constexpr (LF > 0) tmem_store_n<LF>(tPR + O, pr);
-          store_a<CF, L>(tA + O, tAL + O, xm);
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+              const int f = FB + i;
+              if (f < F) {
+                const float m = fmaxf(z[f] - tau, 0.0f);              // sparsemax.py:40
+                pr[i] = pr[i] * (p.gamma - m);                        // network.py:237
+                xm[i] = m * xnv[i];                                   // network.py:238
+                ts_at(f) = m;
+              } else {
+                xm[i] = 0.0f;
+              }
+            }
+            if constexpr (LF > 0) tmem_store_n<LF>(tPR + FB, pr);
+            store_a<CF, L>(tA + FB, tAL + FB, xm);
+          });
+        };
+        if (half == 0) mask_half(std::integral_constant<int, 0>{});
+        else mask_half(std::integral_constant<int, 1>{});
+        if constexpr (CF::DENSE_IO) ptx::fence_async_shared();
+        // shared1 GEMM of step s; masks[s-1] tile goes out meanwhile
+        transform(s, [&] {
+          if (a.masks) flush_rows(a.masks + ((int64_t)(s - 1) * a.rows + r0) * F, nrows);
         });
-        arrive_a();
-        // masks[s-1] tile (network.py:246)
-        if (a.masks) flush_rows(a.masks + ((int64_t)(s - 1) * a.rows + r0) * F, nrows);
-        else ptx::named_bar_sync(bar_id, 128);
-        transform(s);
         // d = relu(f[:, :n_d]); d_sum += d; eta = sum(d); agg += eta*m (network.py:241-245)
-        float eta = 0.0f;
+        if (half == 0) {
+          float eta = 0.0f;
 #pragma unroll
-        for (int j = 0; j < ND; ++j) {
-          const float d = fmaxf(prev[j], 0.0f);
-          dsum[j] += d;
-          eta += d;
+          for (int i = 0; i < HH; ++i) {
+            const float d = fmaxf(prev[i], 0.0f);
+            dsum[i] += d;
+            eta += d;
+          }
+          // While every eta so far is 0, agg holds sum_s m instead (needed only for
+          // the importance fallback, network.py:259-261, which fires exactly then);
+          // the first eta > 0 resets it to eta*m, identical to the reference's sum.
+          const bool reset = all_eta_zero && eta > 0.0f;
+          const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
+          all_eta_zero = all_eta_zero && !(eta > 0.0f);
+          chunked<F>([&](auto o, auto l) {
+            constexpr int O = decltype(o)::value, L = decltype(l)::value;
+            float ag[L];
+            tmem_load_n<L>(tAG + O, ag);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < L; ++i) ag[i] = fmaf(w, ts_at(O + i), reset ? 0.0f : ag[i]);
+            tmem_store_n<L>(tAG + O, ag);
+          });
         }
-        // While every eta so far is 0, agg holds sum_s m instead (it is needed only
-        // for the importance fallback, network.py:259-261, which fires exactly then);
-        // the first eta > 0 resets it to eta*m, identical to the reference's sum.
-        const bool reset = all_eta_zero && eta > 0.0f;
-        const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
-        all_eta_zero = all_eta_zero && !(eta > 0.0f);
-        chunked<F>([&](auto o, auto l) {
-          constexpr int O = decltype(o)::value, L = decltype(l)::value;
-          float ag[L];
-          tmem_load_n<L>(tAG + O, ag);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < L; ++i) ag[i] = fmaf(w, ts_at(O + i), reset ? 0.0f : ag[i]);
-          tmem_store_n<L>(tAG + O, ag);
-        });
       }
-      // ---- head + softmax + argmax (network.py:253-256, :279) ----
-      {
+      // ---- head + softmax + argmax (network.py:253-256, :279), importance
+      // = agg / sum(agg) or mean_s(masks) (network.py:258-261): half 0 ----
+      float ag[F];
+      float div = 1.0f;
+      if (half == 0) {
         float lg[C];
         float lmax = -INFINITY;
 #pragma unroll
@@ -736,9 +741,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         float ex[C], es = 0.0f;
 #pragma unroll
         for (int c = 0; c < C; ++c) { ex[c] = expf(lg[c] - lmax); es += ex[c]; }
-        int best = 0;
-        float bv = -1.0f;
         if (valid) {
+          int best = 0;
+          float bv = -1.0f;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
             const float pv = ex[c] / es;
@@ -748,24 +753,24 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           }
           if (a.pred) a.pred[row] = best;
         }
-      }
-      // ---- importance = agg / sum(agg), or mean_s(masks) (network.py:258-261) ----
-      {
-        float ag[F];
         tmem_load_n<F>(tAG, ag);
         ptx::tmem_ld_wait();
         float tot = 0.0f;
 #pragma unroll
         for (int f = 0; f < F; ++f) tot += ag[f];
-        const float div = all_eta_zero ? (float)S : tot;
-        claim_ts();
+        div = all_eta_zero ? (float)S : tot;
+      }
+      claim_ts();
+      if (half == 0) {
 #pragma unroll
         for (int f = 0; f < F; ++f) ts_at(f) = ag[f] / div;
-        if (a.importance) flush_rows(a.importance + r0 * F, nrows);
       }
+      if constexpr (CF::DENSE_IO) ptx::fence_async_shared();
+      ptx::named_bar_sync(bar_id, 256);
+      if (a.importance) flush_rows(a.importance + r0 * F, nrows);
     }
     if constexpr (CF::DENSE_IO) {
-      if (leader) ptx::bulk_wait0();
+      if (flusher) ptx::bulk_wait0();
     }
   }
 

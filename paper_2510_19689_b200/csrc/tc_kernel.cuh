@@ -397,10 +397,14 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     // tile's sequence -> everyone waits for the accumulator.  `post` runs
     // between the barrier and the wait (overlaps the MMA).
     auto gemm = [&](int j, int64_t pair, auto&& post) {
+      const bool tr = (g == 0 && pair == blockIdx.x);
+      if (tr && issuer) TBN_TRACE(1000 + 4 * j);
+      if (tr && flusher) TBN_TRACE(2000 + 4 * j);
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::named_bar_sync(bar_id, 256);
       if (issuer) {
+        if (tr) TBN_TRACE(1001 + 4 * j);
         ptx::tc_fence_after();
         int kind, step;
         gemm_of(j, kind, step);
@@ -432,11 +436,13 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           }
         }
         ptx::mma_commit(&bars->dfull[g]);
+        if (tr) TBN_TRACE(1002 + 4 * j);
       }
       post();
       ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
       ptx::tc_fence_after();
+      if (tr && issuer) TBN_TRACE(1003 + 4 * j);
     };
     auto nopost = [] {};
 

@@ -234,6 +234,25 @@ __device__ __forceinline__ void store_a_all(uint32_t t_a, uint32_t t_al, const f
   });
 }
 
+// One GEMM's tcgen05.mma chain, fully unrolled: D = A(TMEM, K cols) x B(SMEM,
+// N x K K-major canonical); 3xTF32 adds A_lo x B_hi and A_hi x B_lo.
+template <class CF, int K, int N>
+__device__ __forceinline__ void issue_gemm(uint32_t tD, uint32_t tA, uint32_t tAL, uint32_t bsm) {
+  constexpr uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtTF32, 128, N);
+  constexpr uint32_t sbo = (K / 4) * 128u;
+  constexpr uint64_t lo = (uint64_t)((N * K * 4) >> 4);     // hi -> lo block, in 16 B units
+  const uint64_t d0 = ptx::smem_desc(bsm, 128u, sbo);
+#pragma unroll
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    const uint64_t bd = d0 + (uint64_t)(k0 * 2);             // start address += k0 * 32 B
+    ptx::mma_tf32_ts(tD, tA + k0, bd, idesc, k0 > 0 ? 1u : 0u);
+    if constexpr (CF::X3) {
+      ptx::mma_tf32_ts(tD, tAL + k0, bd, idesc, 1u);
+      ptx::mma_tf32_ts(tD, tA + k0, bd + lo, idesc, 1u);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 template <class CF>
 struct Smem {
@@ -410,33 +429,24 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         gemm_of(j, kind, step);
         const bool res = is_resident<CF>(kind);
         uint32_t bsm;
-        if (j == 0) issue_x(pair + gridDim.x);   // every thread has read this tile's x
+        uint32_t u = 0;
         if (res) {
           bsm = ptx::smem_u32(smem + SM::OFF_RES + (kind == 0 ? 0 : CF::B_SH1));
         } else {
-          const uint32_t u = ring_used++;
+          u = ring_used++;
           ptx::mbar_wait(&bars->wfull[g][u % CF::NSLOT], (u / CF::NSLOT) & 1u);
           bsm = ptx::smem_u32(ring + (u % CF::NSLOT) * CF::SLOT);
-          // block u-1's MMAs completed (its accumulator was waited on): refill
-          // its slot with block u + NSLOT - 1.
-          if (u >= 1) issue_block(u + CF::NSLOT - 1);
         }
-        const int K = kind == 0 ? K1 : (kind == 4 ? NA : H);
-        const int N = kind == 4 ? CF::FN : CF::N2;
-        const uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtTF32, 128, N);
-        const uint32_t sbo = (uint32_t)(K / 4) * 128u;
-        const uint32_t lo_off = (uint32_t)(N * K * 4);
-        for (int k0 = 0; k0 < K; k0 += 8) {
-          const uint64_t bd = ptx::smem_desc(bsm + (uint32_t)k0 * 32u, 128u, sbo);
-          ptx::mma_tf32_ts(tD, tA + k0, bd, idesc, k0 > 0 ? 1u : 0u);
-          if constexpr (CF::X3) {
-            const uint64_t bdl = ptx::smem_desc(bsm + lo_off + (uint32_t)k0 * 32u, 128u, sbo);
-            ptx::mma_tf32_ts(tD, tAL + k0, bd, idesc, 1u);
-            ptx::mma_tf32_ts(tD, tA + k0, bdl, idesc, 1u);
-          }
-        }
+        if (kind == 0) issue_gemm<CF, K1, CF::N2>(tD, tA, tAL, bsm);
+        else if (kind == 4) issue_gemm<CF, NA, CF::FN>(tD, tA, tAL, bsm);
+        else issue_gemm<CF, H, CF::N2>(tD, tA, tAL, bsm);
         ptx::mma_commit(&bars->dfull[g]);
         if (tr) TBN_TRACE(1002 + 4 * j);
+        // producer duties, off the MMA critical path: next x tile once every
+        // thread has read this one; refill the slot of ring block u-1 (its MMAs
+        // completed: their accumulator was waited on) with block u + NSLOT - 1.
+        if (j == 0) issue_x(pair + gridDim.x);
+        if (!res && u >= 1) issue_block(u + CF::NSLOT - 1);
       }
       post();
       ptx::mbar_wait(&bars->dfull[g], dphase);
@@ -616,6 +626,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         // A <- a = f[:, n_d:]  (half 1 owns it)
         if (half == 1) store_a_all<CF, NA>(tA, tAL, prev);
         gemm(j++, pair, nopost);
+        const bool trs = (g == 0 && pair == blockIdx.x && issuer);
+        if (trs) TBN_TRACE(3000 + 8 * s);
         // attentive FC + prior + sparsemax (network.py:233-236, sparsemax.py:13-41)
         float z[F];
         const float* batt = cst + CF::C_BATT + (s - 1) * CF::FN;
@@ -634,6 +646,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         });
 #pragma unroll
         for (int f = 0; f < F; ++f) z[f] -= zmax;                     // sparsemax.py:32
+        if (trs) TBN_TRACE(3001 + 8 * s);
         // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
         // monotone from any lower bound of tau*; its support equals the
         // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
@@ -666,7 +679,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           cnt_prev = c;
           tau = __fdiv_rn(sm - 1.0f, c);                              // sparsemax.py:39
         }
+        if (trs) TBN_TRACE(3002 + 8 * s);
         claim_ts();
+        if (trs) TBN_TRACE(3003 + 8 * s);
         // this half's features: mask, prior update, xm -> A (network.py:237-238, :246)
         auto mask_half = [&](auto hc) {
           constexpr int HB = decltype(hc)::value;
@@ -698,6 +713,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         };
         if (half == 0) mask_half(std::integral_constant<int, 0>{});
         else mask_half(std::integral_constant<int, 1>{});
+        if (trs) TBN_TRACE(3004 + 8 * s);
         if constexpr (CF::DENSE_IO) ptx::fence_async_shared();
         // shared1 GEMM of step s; masks[s-1] tile goes out meanwhile
         transform(s, [&] {

@@ -422,8 +422,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::named_bar_sync(bar_id, 256);
-      if (issuer) {
-        if (tr) TBN_TRACE(1001 + 4 * j);
+      if ((warp & 7) == 0) {                     // the group's issuing warp, converged
+        if (tr && issuer) TBN_TRACE(1001 + 4 * j);
         ptx::tc_fence_after();
         int kind, step;
         gemm_of(j, kind, step);
@@ -441,12 +441,14 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         else if (kind == 4) issue_gemm<CF, NA, CF::FN>(tD, tA, tAL, bsm);
         else issue_gemm<CF, H, CF::N2>(tD, tA, tAL, bsm);
         ptx::mma_commit(&bars->dfull[g]);
-        if (tr) TBN_TRACE(1002 + 4 * j);
+        if (tr && issuer) TBN_TRACE(1002 + 4 * j);
         // producer duties, off the MMA critical path: next x tile once every
         // thread has read this one; refill the slot of ring block u-1 (its MMAs
         // completed: their accumulator was waited on) with block u + NSLOT - 1.
-        if (j == 0) issue_x(pair + gridDim.x);
-        if (!res && u >= 1) issue_block(u + CF::NSLOT - 1);
+        if (issuer) {
+          if (j == 0) issue_x(pair + gridDim.x);
+          if (!res && u >= 1) issue_block(u + CF::NSLOT - 1);
+        }
       }
       post();
       ptx::mbar_wait(&bars->dfull[g], dphase);

@@ -402,7 +402,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         ptx::mbar_arrive(&bars->xfull[g]);
       }
     };
-    uint32_t ring_used = 0;                   // issuer-only: ring blocks consumed
+    uint32_t ring_used = 0;                   // issuing warp: ring blocks consumed
+    uint32_t ring_issued = 0;                 // flusher: ring blocks seen (refill cursor)
     if (issuer) {
       issue_x(blockIdx.x);
       for (uint32_t u = 0; u < (uint32_t)CF::NSLOT; ++u) issue_block(u);
@@ -422,6 +423,19 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::named_bar_sync(bar_id, 256);
+      if (flusher) {
+        // Producer duties, off the MMA-issue path.  Every GEMM before j has
+        // completed (all threads waited on its accumulator), so the slot of
+        // ring block u-1 is free: refill it with block u + NSLOT - 1.  At j == 0
+        // every thread has read this tile's x: prefetch the group's next tile.
+        int kind, step;
+        gemm_of(j, kind, step);
+        if (!is_resident<CF>(kind)) {
+          const uint32_t u = ring_issued++;
+          if (u >= 1) issue_block(u + CF::NSLOT - 1);
+        }
+        if (j == 0) issue_x(pair + gridDim.x);
+      }
       if ((warp & 7) == 0) {                     // the group's issuing warp, converged
         if (tr && issuer) TBN_TRACE(1001 + 4 * j);
         ptx::tc_fence_after();
@@ -442,13 +456,6 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         else issue_gemm<CF, H, CF::N2>(tD, tA, tAL, bsm);
         ptx::mma_commit(&bars->dfull[g]);
         if (tr && issuer) TBN_TRACE(1002 + 4 * j);
-        // producer duties, off the MMA critical path: next x tile once every
-        // thread has read this one; refill the slot of ring block u-1 (its MMAs
-        // completed: their accumulator was waited on) with block u + NSLOT - 1.
-        if (issuer) {
-          if (j == 0) issue_x(pair + gridDim.x);
-          if (!res && u >= 1) issue_block(u + CF::NSLOT - 1);
-        }
       }
       post();
       ptx::mbar_wait(&bars->dfull[g], dphase);
@@ -664,14 +671,21 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         }
         float cnt_prev = (float)(F + 1);
         for (int it = 0; it <= F; ++it) {
-          float2 sm2 = f2(0.0f, 0.0f), c2 = f2(0.0f, 0.0f);
+          // 4 independent (sum, count) pairs keep the dependency chains short
+          float2 sa = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
 #pragma unroll
           for (int f = 0; f + 1 < F; f += 2) {
             const float2 m = f2(z[f] > tau ? 1.0f : 0.0f, z[f + 1] > tau ? 1.0f : 0.0f);
-            sm2 = __ffma2_rn(m, f2(z[f], z[f + 1]), sm2);
-            c2 = __fadd2_rn(c2, m);
+            if ((f / 2) % 2 == 0) {
+              sa = __ffma2_rn(m, f2(z[f], z[f + 1]), sa);
+              ca = __fadd2_rn(ca, m);
+            } else {
+              sb = __ffma2_rn(m, f2(z[f], z[f + 1]), sb);
+              cb = __fadd2_rn(cb, m);
+            }
           }
-          float sm = sm2.x + sm2.y, c = c2.x + c2.y;
+          const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
+          float sm = s2.x + s2.y, c = c2.x + c2.y;
           if constexpr (F % 2) {
             const float m = z[F - 1] > tau ? 1.0f : 0.0f;
             sm = fmaf(m, z[F - 1], sm);
@@ -679,7 +693,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           }
           if (c >= cnt_prev) break;
           cnt_prev = c;
-          tau = __fdiv_rn(sm - 1.0f, c);                              // sparsemax.py:39
+          tau = __fdividef(sm - 1.0f, c);                             // sparsemax.py:39
         }
         if (trs) TBN_TRACE(3002 + 8 * s);
         claim_ts();

@@ -27,6 +27,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
           f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-v", "--expt-relaxed-constexpr",
                             "-Xcompiler", "-Wall"]
+if os.environ.get("TBN_TRACE_BUILD"):          # development timeline build (see tools/trace_run.py)
+    CU_FLAGS += ["-DTBN_ENABLE_TRACE"]
 CXX = shutil.which("g++") or "g++"
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 

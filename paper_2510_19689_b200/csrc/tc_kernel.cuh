@@ -79,7 +79,7 @@ struct Cfg {
   static constexpr bool DENSE_IO = (F % 2 == 1) || (F <= 16);
   static constexpr int XSTAGE = rup(128 * F * 4, 128);
   static constexpr int TSTAGE = DENSE_IO ? rup(128 * F * 4, 128) : rup(F * 129 * 4, 128);
-  static constexpr int FIXED = rup(CONST_BYTES, 128) + NG * (XSTAGE + TSTAGE) + 1024;
+  static constexpr int FIXED = rup(CONST_BYTES, 128) + NG * (XSTAGE + TSTAGE + 4096) + 1024;
   static constexpr int RING_SLOT_ALL = cmax(cmax(B_SH1, B_HID), B_ATT);
   static constexpr int RING_SLOT_RES = cmax(B_HID, B_ATT);
   static constexpr int SMEM_BUDGET = 225 * 1024;
@@ -201,25 +201,26 @@ __device__ __forceinline__ void chunked(Fn&& fn) {
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-// Write L columns of an A operand row to TMEM: hi = rna_tf32(v), lo = v - hi
-// (3xTF32), or v as is (the tensor core truncates fp32 to tf32).
+// Write L columns of an A operand row to TMEM.  The tensor core reads fp32
+// operands as tf32 by truncation, so A_hi = v itself (read as trunc(v)) and,
+// for 3xTF32, A_lo = v - trunc(v) (exact in fp32; itself truncated by the MMA,
+// leaving a 2^-22 relative error per product).
 template <class CF, int L, int M>
 __device__ __forceinline__ void store_a(uint32_t t_a, uint32_t t_al, const float (&v)[M]) {
+  tmem_store_n<L>(t_a, v);
   if constexpr (CF::X3) {
-    float hi[L], lo[L];
-#pragma unroll
-    for (int i = 0; i < L; ++i) hi[i] = tf32_rna(v[i]);
+    float lo[L];
 #pragma unroll
     for (int i = 0; i + 1 < L; i += 2) {
-      const float2 d = __fadd2_rn(f2(v[i], v[i + 1]), f2(-hi[i], -hi[i + 1]));
+      const float2 d = __fadd2_rn(f2(v[i], v[i + 1]),
+                                  f2(-__uint_as_float(__float_as_uint(v[i]) & 0xFFFFE000u),
+                                     -__uint_as_float(__float_as_uint(v[i + 1]) & 0xFFFFE000u)));
       lo[i] = d.x;
       lo[i + 1] = d.y;
     }
-    if constexpr (L % 2) lo[L - 1] = v[L - 1] - hi[L - 1];
-    tmem_store_n<L>(t_a, hi);
+    if constexpr (L % 2)
+      lo[L - 1] = v[L - 1] - __uint_as_float(__float_as_uint(v[L - 1]) & 0xFFFFE000u);
     tmem_store_n<L>(t_al, lo);
-  } else {
-    tmem_store_n<L>(t_a, v);
   }
 }
 // A <- v[0..K) in 16-column chunks
@@ -261,7 +262,8 @@ struct Smem {
   static constexpr int OFF_T = OFF_X + CF::NG * CF::XSTAGE;
   static constexpr int OFF_RES = rup(OFF_T + CF::NG * CF::TSTAGE, 1024);
   static constexpr int OFF_RING = OFF_RES + CF::RES_BYTES;
-  static constexpr int OFF_BAR = OFF_RING + CF::NG * CF::NSLOT * CF::SLOT;
+  static constexpr int OFF_XCH = OFF_RING + CF::NG * CF::NSLOT * CF::SLOT;   // 4 KB per group
+  static constexpr int OFF_BAR = OFF_XCH + CF::NG * 4096;
   static constexpr int TOTAL = OFF_BAR + 256;
   static_assert(TOTAL <= 227 * 1024, "smem");
 };
@@ -320,11 +322,18 @@ __device__ __forceinline__ bool is_resident(int kind) {
 }
 
 // ---------------------------------------------------------------------------
-// Debug timeline: slot k of CTA 0 <- clock64 (only when a.trace is set).
+// Debug timeline (build with -DTBN_ENABLE_TRACE and run with TBN_TRACE=1):
+// slot k of CTA 0 <- clock64.  Compiled out of production builds.
+#ifdef TBN_ENABLE_TRACE
 #define TBN_TRACE(k)                                                        \
   do {                                                                      \
     if (a.trace && blockIdx.x == 0 && (k) < 4096) a.trace[(k)] = clock64(); \
   } while (0)
+#else
+#define TBN_TRACE(k) \
+  do {               \
+  } while (0)
+#endif
 
 template <class CF>
 __global__ void __launch_bounds__(CF::THREADS, 1)
@@ -530,6 +539,18 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       }
       ptx::named_bar_sync(bar_id, 256);
     };
+    // (a, b) exchange with the partner warp of the same lane quarter (the other
+    // column half): double-buffered by parity, one 64-thread barrier each.
+    float2* xbuf = reinterpret_cast<float2*>(smem + SM::OFF_XCH) + g * 512;
+    const uint32_t pair_bar = 3 + g * 4 + (warp & 3);
+    uint32_t xpar = 0;
+    auto xchg = [&](float va, float vb) -> float2 {
+      xbuf[(xpar * 2 + half) * 128 + t] = f2(va, vb);
+      ptx::named_bar_sync(pair_bar, 64);
+      const float2 o = xbuf[(xpar * 2 + (half ^ 1)) * 128 + t];
+      xpar ^= 1;
+      return o;
+    };
     auto ts_at = [&](int f) -> float& {
       if constexpr (CF::DENSE_IO) return ts[t * F + f];
       else return ts[f * 129 + t];
@@ -637,73 +658,79 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         gemm(j++, pair, nopost);
         const bool trs = (g == 0 && pair == blockIdx.x && issuer);
         if (trs) TBN_TRACE(3000 + 8 * s);
-        // attentive FC + prior + sparsemax (network.py:233-236, sparsemax.py:13-41)
-        float z[F];
-        const float* batt = cst + CF::C_BATT + (s - 1) * CF::FN;
-        float zmax = -INFINITY;
-        chunked<F>([&](auto o, auto l) {
-          constexpr int O = decltype(o)::value, L = decltype(l)::value;
-          float pr[L];
-          tmem_load_n<L, O>(tD + O, z);
-          tmem_load_n<L>(tPR + O, pr);
-          ptx::tmem_ld_wait();
+        // attentive FC + prior + sparsemax (network.py:233-236, sparsemax.py:13-41),
+        // features split between the two halves; the row's (max, sum, count)
+        // reductions are combined through SMEM with the partner warp (a 64-thread
+        // barrier per exchange).  a+b == b+a in IEEE, so both halves hold
+        // bitwise-identical combined values and take identical decisions.
+        auto attentive = [&](auto hc) {
+          constexpr int HB = decltype(hc)::value * KH;             // first feature
+          constexpr int FE = (HB + KH < F) ? HB + KH : F;
+          constexpr int NF = FE > HB ? FE - HB : 0;               // own features
+          float z[NF > 0 ? NF : 1];
+          const float* batt = cst + CF::C_BATT + (s - 1) * CF::FN + HB;
+          float zmax = -INFINITY;
+          chunked<NF>([&](auto o, auto l) {
+            constexpr int O = decltype(o)::value, L = decltype(l)::value;
+            float pr[L];
+            tmem_load_n<L, O>(tD + HB + O, z);
+            tmem_load_n<L>(tPR + HB + O, pr);
+            ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < L; ++i) {
-            z[O + i] = pr[i] * (z[O + i] + batt[O + i]);            // network.py:233-235
-            zmax = fmaxf(zmax, z[O + i]);
-          }
-        });
-#pragma unroll
-        for (int f = 0; f < F; ++f) z[f] -= zmax;                     // sparsemax.py:32
-        if (trs) TBN_TRACE(3001 + 8 * s);
-        // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
-        // monotone from any lower bound of tau*; its support equals the
-        // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
-        // max(-1, (sum z - 1)/F): both bound tau* from below.
-        float tau;
-        {
-          float2 acc = f2(0.0f, 0.0f);
-#pragma unroll
-          for (int f = 0; f + 1 < F; f += 2) acc = __fadd2_rn(acc, f2(z[f], z[f + 1]));
-          float tot = acc.x + acc.y;
-          if constexpr (F % 2) tot += z[F - 1];
-          tau = fmaxf(-1.0f, (tot - 1.0f) * (1.0f / (float)F));
-        }
-        float cnt_prev = (float)(F + 1);
-        for (int it = 0; it <= F; ++it) {
-          // 4 independent (sum, count) pairs keep the dependency chains short
-          float2 sa = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
-#pragma unroll
-          for (int f = 0; f + 1 < F; f += 2) {
-            const float2 m = f2(z[f] > tau ? 1.0f : 0.0f, z[f + 1] > tau ? 1.0f : 0.0f);
-            if ((f / 2) % 2 == 0) {
-              sa = __ffma2_rn(m, f2(z[f], z[f + 1]), sa);
-              ca = __fadd2_rn(ca, m);
-            } else {
-              sb = __ffma2_rn(m, f2(z[f], z[f + 1]), sb);
-              cb = __fadd2_rn(cb, m);
+            for (int i = 0; i < L; ++i) {
+              z[O + i] = pr[i] * (z[O + i] + batt[O + i]);          // network.py:233-235
+              zmax = fmaxf(zmax, z[O + i]);
             }
+          });
+          zmax = fmaxf(zmax, xchg(zmax, 0.0f).x);
+          float own = 0.0f;
+#pragma unroll
+          for (int i = 0; i < NF; ++i) {
+            z[i] -= zmax;                                           // sparsemax.py:32
+            own += z[i];
           }
-          const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
-          float sm = s2.x + s2.y, c = c2.x + c2.y;
-          if constexpr (F % 2) {
-            const float m = z[F - 1] > tau ? 1.0f : 0.0f;
-            sm = fmaf(m, z[F - 1], sm);
-            c += m;
+          if (trs) TBN_TRACE(3001 + 8 * s);
+          // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
+          // monotone from any lower bound of tau*; its support equals the
+          // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
+          // max(-1, (sum z - 1)/F): both bound tau* from below.
+          float tau = fmaxf(-1.0f, ((own + xchg(own, 0.0f).x) - 1.0f) * (1.0f / (float)F));
+          float cnt_prev = (float)(F + 1);
+          for (int it = 0; it <= F; ++it) {
+            float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
+#pragma unroll
+            for (int i = 0; i + 1 < NF; i += 2) {
+              const float2 m = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
+              if ((i / 2) % 2 == 0) {
+                sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
+                ca = __fadd2_rn(ca, m);
+              } else {
+                sb = __ffma2_rn(m, f2(z[i], z[i + 1]), sb);
+                cb = __fadd2_rn(cb, m);
+              }
+            }
+            const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
+            float sm = s2.x + s2.y, c = c2.x + c2.y;
+            if constexpr (NF % 2) {
+              const float m = z[NF - 1] > tau ? 1.0f : 0.0f;
+              sm = fmaf(m, z[NF - 1], sm);
+              c += m;
+            }
+            const float2 o = xchg(sm, c);
+            sm += o.x;
+            c += o.y;
+            if (c >= cnt_prev) break;
+            cnt_prev = c;
+            tau = __fdividef(sm - 1.0f, c);                           // sparsemax.py:39
           }
-          if (c >= cnt_prev) break;
-          cnt_prev = c;
-          tau = __fdividef(sm - 1.0f, c);                             // sparsemax.py:39
-        }
-        if (trs) TBN_TRACE(3002 + 8 * s);
-        claim_ts();
-        if (trs) TBN_TRACE(3003 + 8 * s);
-        // this half's features: mask, prior update, xm -> A (network.py:237-238, :246)
-        auto mask_half = [&](auto hc) {
-          constexpr int HB = decltype(hc)::value;
+          if (trs) TBN_TRACE(3002 + 8 * s);
+          claim_ts();
+          if (trs) TBN_TRACE(3003 + 8 * s);
+          // own features: mask, prior update, xm -> A (network.py:237-238, :246);
+          // A columns [HB, HB + KH) incl. zero padding up to K1
           chunked<KH>([&](auto o, auto l) {
             constexpr int O = decltype(o)::value, L = decltype(l)::value;
-            constexpr int FB = HB * KH + O;
+            constexpr int FB = HB + O;
             constexpr int LF = (FB + L <= F) ? L : (FB < F ? F - FB : 0);
             float pr[L], xnv[L], xm[L];
             if constexpr (LF > 0) {
@@ -715,7 +742,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
             for (int i = 0; i < L; ++i) {
               const int f = FB + i;
               if (f < F) {
-                const float m = fmaxf(z[f] - tau, 0.0f);              // sparsemax.py:40
+                const float m = fmaxf(z[O + i] - tau, 0.0f);          // sparsemax.py:40
                 pr[i] = pr[i] * (p.gamma - m);                        // network.py:237
                 xm[i] = m * xnv[i];                                   // network.py:238
                 ts_at(f) = m;
@@ -726,10 +753,10 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
             if constexpr (LF > 0) tmem_store_n<LF>(tPR + FB, pr);
             store_a<CF, L>(tA + FB, tAL + FB, xm);
           });
+          if (trs) TBN_TRACE(3004 + 8 * s);
         };
-        if (half == 0) mask_half(std::integral_constant<int, 0>{});
-        else mask_half(std::integral_constant<int, 1>{});
-        if (trs) TBN_TRACE(3004 + 8 * s);
+        if (half == 0) attentive(std::integral_constant<int, 0>{});
+        else attentive(std::integral_constant<int, 1>{});
         if constexpr (CF::DENSE_IO) ptx::fence_async_shared();
         // shared1 GEMM of step s; masks[s-1] tile goes out meanwhile
         transform(s, [&] {
@@ -764,7 +791,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       // ---- head + softmax + argmax (network.py:253-256, :279), importance
       // = agg / sum(agg) or mean_s(masks) (network.py:258-261): half 0 ----
       float ag[F];
-      float div = 1.0f;
+      float div = 1.0f, rdiv = 1.0f;
       if (half == 0) {
         float lg[C];
         float lmax = -INFINITY;
@@ -797,11 +824,12 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
 #pragma unroll
         for (int f = 0; f < F; ++f) tot += ag[f];
         div = all_eta_zero ? (float)S : tot;
+        rdiv = __frcp_rn(div);
       }
       claim_ts();
       if (half == 0) {
 #pragma unroll
-        for (int f = 0; f < F; ++f) ts_at(f) = ag[f] / div;
+        for (int f = 0; f < F; ++f) ts_at(f) = ag[f] * rdiv;
       }
       if constexpr (CF::DENSE_IO) ptx::fence_async_shared();
       ptx::named_bar_sync(bar_id, 256);

@@ -695,7 +695,11 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
           // max(-1, (sum z - 1)/F): both bound tau* from below.
           float tau = fmaxf(-1.0f, ((own + xchg(own, 0.0f).x) - 1.0f) * (1.0f / (float)F));
+          // The loop runs warp-uniformly (bar.sync inside must be executed by
+          // whole warps): a converged row keeps its tau until all 32 rows of the
+          // warp — the same rows as the partner warp — have converged.
           float cnt_prev = (float)(F + 1);
+          bool done = false;
           for (int it = 0; it <= F; ++it) {
             float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
 #pragma unroll
@@ -719,9 +723,15 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
             const float2 o = xchg(sm, c);
             sm += o.x;
             c += o.y;
-            if (c >= cnt_prev) break;
-            cnt_prev = c;
-            tau = __fdividef(sm - 1.0f, c);                           // sparsemax.py:39
+            if (!done) {
+              if (c >= cnt_prev) {
+                done = true;
+              } else {
+                cnt_prev = c;
+                tau = __fdividef(sm - 1.0f, c);                       // sparsemax.py:39
+              }
+            }
+            if (__all_sync(0xffffffffu, done)) break;
           }
           if (trs) TBN_TRACE(3002 + 8 * s);
           claim_ts();

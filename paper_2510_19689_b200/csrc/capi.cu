@@ -274,8 +274,8 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
   static const bool trace_on = getenv("TBN_TRACE") != nullptr;
   static unsigned long long* d_trace = nullptr;
   if (trace_on && m->precision != TBN_PREC_FP32) {
-    if (!d_trace) cudaMalloc(&d_trace, 4096 * sizeof(unsigned long long));
-    cudaMemsetAsync(d_trace, 0, 4096 * sizeof(unsigned long long), s);
+    if (!d_trace) cudaMalloc(&d_trace, 16384 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_trace, 0, 16384 * sizeof(unsigned long long), s);
     a.trace = d_trace;
   }
   cudaError_t e;
@@ -285,12 +285,12 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
     e = tbn::launch_tc(m->tc, a, m->num_sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
   if (a.trace) {
-    std::vector<unsigned long long> h(4096);
-    cudaMemcpyAsync(h.data(), d_trace, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    std::vector<unsigned long long> h(16384);
+    cudaMemcpyAsync(h.data(), d_trace, 16384 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     const unsigned long long t0 = h[0];
     fprintf(stderr, "TRACE rows=%lld\n", (long long)rows);
-    for (int k = 0; k < 4096; ++k)
+    for (int k = 0; k < 16384; ++k)
       if (h[k]) fprintf(stderr, "TRACE %d %lld\n", k, (long long)(h[k] - t0));
   }
   return TBN_OK;

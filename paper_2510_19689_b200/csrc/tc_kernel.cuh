@@ -327,7 +327,7 @@ __device__ __forceinline__ bool is_resident(int kind) {
 #ifdef TBN_ENABLE_TRACE
 #define TBN_TRACE(k)                                                        \
   do {                                                                      \
-    if (a.trace && blockIdx.x == 0 && (k) < 4096) a.trace[(k)] = clock64(); \
+    if (a.trace && blockIdx.x == 0 && (k) < 16384) a.trace[(k)] = clock64(); \
   } while (0)
 #else
 #define TBN_TRACE(k) \
@@ -426,9 +426,10 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     // tile's sequence -> everyone waits for the accumulator.  `post` runs
     // between the barrier and the wait (overlaps the MMA).
     auto gemm = [&](int j, int64_t pair, auto&& post) {
-      const bool tr = (g == 0 && pair == blockIdx.x);
-      if (tr && issuer) TBN_TRACE(1000 + 4 * j);
-      if (tr && flusher) TBN_TRACE(2000 + 4 * j);
+      const bool tr = (pair == blockIdx.x);
+      const int gofs = g * 5000;
+      if (tr && issuer) TBN_TRACE(gofs + 1000 + 4 * j);
+      if (tr && flusher) TBN_TRACE(gofs + 2000 + 4 * j);
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::named_bar_sync(bar_id, 256);
@@ -446,7 +447,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         if (j == 0) issue_x(pair + gridDim.x);
       }
       if ((warp & 7) == 0) {                     // the group's issuing warp, converged
-        if (tr && issuer) TBN_TRACE(1001 + 4 * j);
+        if (tr && issuer) TBN_TRACE(gofs + 1001 + 4 * j);
         ptx::tc_fence_after();
         int kind, step;
         gemm_of(j, kind, step);
@@ -464,13 +465,13 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         else if (kind == 4) issue_gemm<CF, NA, CF::FN>(tD, tA, tAL, bsm);
         else issue_gemm<CF, H, CF::N2>(tD, tA, tAL, bsm);
         ptx::mma_commit(&bars->dfull[g]);
-        if (tr && issuer) TBN_TRACE(1002 + 4 * j);
+        if (tr && issuer) TBN_TRACE(gofs + 1002 + 4 * j);
       }
       post();
       ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
       ptx::tc_fence_after();
-      if (tr && issuer) TBN_TRACE(1003 + 4 * j);
+      if (tr && issuer) TBN_TRACE(gofs + 1003 + 4 * j);
     };
     auto nopost = [] {};
 

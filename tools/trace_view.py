@@ -9,9 +9,10 @@ for fn in sys.argv[1:]:
             d[int(p[1])] = int(p[2])
     print(fn, 'end', d.get(2))
     prev_end = None
+    G = int(__import__("os").environ.get("TG", "0")) * 5000
     for j in range(64):
-        a0, a1, a2, a3, f0 = (d.get(1000 + 4 * j), d.get(1001 + 4 * j), d.get(1002 + 4 * j),
-                              d.get(1003 + 4 * j), d.get(2000 + 4 * j))
+        a0, a1, a2, a3, f0 = (d.get(G + 1000 + 4 * j), d.get(G + 1001 + 4 * j), d.get(G + 1002 + 4 * j),
+                              d.get(G + 1003 + 4 * j), d.get(G + 2000 + 4 * j))
         if a0 is None or a1 is None:
             continue
         f0 = f0 or a0

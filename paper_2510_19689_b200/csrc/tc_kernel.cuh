@@ -426,6 +426,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     // tile's sequence -> everyone waits for the accumulator.  `post` runs
     // between the barrier and the wait (overlaps the MMA).
     auto gemm = [&](int j, int64_t pair, auto&& post) {
+      seg_release();
       const bool tr = (pair == blockIdx.x);
       const int gofs = g * 5000;
       if (tr && issuer) TBN_TRACE(gofs + 1000 + 4 * j);
@@ -471,6 +472,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
       ptx::tc_fence_after();
+      seg_acquire(false);
       if (tr && issuer) TBN_TRACE(gofs + 1003 + 4 * j);
     };
     auto nopost = [] {};
@@ -552,6 +554,17 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       xpar ^= 1;
       return o;
     };
+    // Ping-pong token (FA4 style): the two row groups' CUDA-core segments (the
+    // work between two GEMMs) strictly alternate, so each group's tcgen05 MMAs
+    // run while the other group computes.  Named barrier 11+g = "group g may
+    // run its next segment"; the other group arrives on it when its segment ends.
+    bool paired = false;        // both groups have a tile in the current pair
+    auto seg_acquire = [&](bool first_of_pair) {
+      if (paired && !(g == 0 && first_of_pair)) ptx::named_bar_sync(11 + g, 512);
+    };
+    auto seg_release = [&]() {
+      if (paired) ptx::named_bar_arrive(11 + (g ^ 1), 512);
+    };
     auto ts_at = [&](int f) -> float& {
       if constexpr (CF::DENSE_IO) return ts[t * F + f];
       else return ts[f * 129 + t];
@@ -570,6 +583,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       // half's features (network.py:118-120); prior = 1; agg = 0 ----
       ptx::mbar_wait(&bars->xfull[g], xphase);
       xphase ^= 1;
+      paired = (NG == 2) && (pair * NG + 1 < ntiles);
+      seg_acquire(true);
       {
         const int ne = nrows * F;
         const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
@@ -845,6 +860,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       if constexpr (CF::DENSE_IO) ptx::fence_async_shared();
       ptx::named_bar_sync(bar_id, 256);
       if (a.importance) flush_rows(a.importance + r0 * F, nrows);
+      seg_release();
+      if (paired && g == 0) ptx::named_bar_sync(11, 512);   // consume group 1's last handoff
     }
     if constexpr (CF::DENSE_IO) {
       if (flusher) ptx::bulk_wait0();

@@ -422,6 +422,17 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     const float* shift = a.shift ? a.shift : cst + CF::C_SHIFT;
     uint32_t xphase = 0, dphase = 0;
 
+    // Ping-pong token (FA4 style): the two row groups' CUDA-core segments (the
+    // work between two GEMMs) strictly alternate, so each group's tcgen05 MMAs
+    // run while the other group computes.  Named barrier 11+g = "group g may
+    // run its next segment"; the other group arrives on it when its segment ends.
+    bool paired = false;        // both groups have a tile in the current pair
+    auto seg_acquire = [&](bool first_of_pair) {
+      if (paired && !(g == 0 && first_of_pair)) ptx::named_bar_sync(11 + g, 512);
+    };
+    auto seg_release = [&]() {
+      if (paired) ptx::named_bar_arrive(11 + (g ^ 1), 512);
+    };
     // A is written (both halves) -> barrier -> one thread issues GEMM j of the
     // tile's sequence -> everyone waits for the accumulator.  `post` runs
     // between the barrier and the wait (overlaps the MMA).
@@ -553,17 +564,6 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       const float2 o = xbuf[(xpar * 2 + (half ^ 1)) * 128 + t];
       xpar ^= 1;
       return o;
-    };
-    // Ping-pong token (FA4 style): the two row groups' CUDA-core segments (the
-    // work between two GEMMs) strictly alternate, so each group's tcgen05 MMAs
-    // run while the other group computes.  Named barrier 11+g = "group g may
-    // run its next segment"; the other group arrives on it when its segment ends.
-    bool paired = false;        // both groups have a tile in the current pair
-    auto seg_acquire = [&](bool first_of_pair) {
-      if (paired && !(g == 0 && first_of_pair)) ptx::named_bar_sync(11 + g, 512);
-    };
-    auto seg_release = [&]() {
-      if (paired) ptx::named_bar_arrive(11 + (g ^ 1), 512);
     };
     auto ts_at = [&](int f) -> float& {
       if constexpr (CF::DENSE_IO) return ts[t * F + f];

@@ -7,7 +7,8 @@ Training (``train``/``accuracy``/``roc_auc``) is out of scope
 """
 from .config import ModelConfig
 from .errors import (ChecksumError, ConfigurationError, DeviceError, FormatVersionError,
-                     InvalidInputError, ModelFormatError, TabserveError, TruncatedStreamError)
+                     InvalidInputError, ModelFormatError, TabserveError, TruncatedStreamError,
+                     UnsupportedShapeError)
 from .network import (DEFAULT_PRECISION, Explanation, ForwardResult, GpuTabNetModel,
                       PredictionOutput, TabNetModel, init_parameters)
 from .sparsemax import project_simplex_bruteforce, sparsemax
@@ -21,4 +22,5 @@ __all__ = [
     "save_model", "load_model", "save_model_file", "load_model_file", "DEFAULT_PRECISION",
     "TabserveError", "InvalidInputError", "ConfigurationError", "ModelFormatError",
     "FormatVersionError", "TruncatedStreamError", "ChecksumError", "DeviceError",
+    "UnsupportedShapeError",
 ]

@@ -12,7 +12,8 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import ConfigurationError, DeviceError, InvalidInputError, TabserveError
+from .errors import (ConfigurationError, DeviceError, InvalidInputError, TabserveError,
+                     UnsupportedShapeError)
 
 LIB_PATH = Path(__file__).resolve().parent / "libtabnet_b200.so"
 
@@ -105,7 +106,9 @@ def check(status: int, what: str = "") -> None:
         raise InvalidInputError(msg)
     if status == TBN_ERR_CONFIG:
         raise ConfigurationError(msg)
-    if status in (TBN_ERR_CUDA, TBN_ERR_UNSUPPORTED):
+    if status == TBN_ERR_UNSUPPORTED:
+        raise UnsupportedShapeError(msg)
+    if status == TBN_ERR_CUDA:
         raise DeviceError(msg)
     raise TabserveError(f"status {status}: {msg}")
 

@@ -23,11 +23,15 @@ import numpy as np
 
 from . import _native as N
 from .config import ModelConfig
-from .errors import ConfigurationError, InvalidInputError
+from .errors import ConfigurationError, InvalidInputError, UnsupportedShapeError
 
 _NORM_EPS = 1e-8
 _RESIDUAL_SCALE = math.sqrt(0.5)
-DEFAULT_PRECISION = "tf32x3"
+DEFAULT_PRECISION = "auto"
+# "auto": the fused tcgen05 kernel in 3xTF32 (fp32-faithful) where an instance
+# is compiled for the model shape, else the fp32 CUDA-core kernel.  Both are GPU
+# kernels; neither is a CPU fallback.
+AUTO_ORDER = ("tf32x3", "fp32")
 
 
 @dataclass
@@ -173,7 +177,7 @@ class TabNetModel:
             raise ConfigurationError("model_version must be non-empty")
         if np.any(np.asarray(self.norm_var) <= 0):
             raise ConfigurationError("normalization variances must be > 0")
-        if self.precision not in N.PRECISIONS:
+        if self.precision not in N.PRECISIONS and self.precision != "auto":
             raise ConfigurationError(f"unknown precision {self.precision!r}")
         self._engines: dict = {}
         self._engine_lock = threading.Lock()
@@ -203,8 +207,17 @@ class TabNetModel:
             with self._engine_lock:
                 eng = self._engines.get(key)
                 if eng is None:
-                    eng = DeviceModel(self.config, self.params, self.norm_mean, self.norm_var,
-                                      prec, dev)
+                    if prec == "auto":
+                        for cand in AUTO_ORDER:
+                            try:
+                                eng = DeviceModel(self.config, self.params, self.norm_mean,
+                                                  self.norm_var, cand, dev)
+                                break
+                            except UnsupportedShapeError:
+                                continue
+                    else:
+                        eng = DeviceModel(self.config, self.params, self.norm_mean, self.norm_var,
+                                          prec, dev)
                     self._engines[key] = eng
         return eng
 

@@ -437,7 +437,13 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     // tile's sequence -> everyone waits for the accumulator.  `post` runs
     // between the barrier and the wait (overlaps the MMA).
     auto gemm = [&](int j, int64_t pair, auto&& post) {
-      seg_release();
+      // The attentive segment (after an att GEMM, j = 4 + 5(s-1)) is latency-
+      // bound (sparsemax iterations): both groups run theirs outside the token,
+      // overlapping each other.  Both skip the same segment, so the alternation
+      // parity is preserved.
+      const bool after_att = (j >= 5) && ((j - 5) % 5 == 0);
+      const bool is_att = (j >= 4) && ((j - 4) % 5 == 0);
+      if (!after_att) seg_release();
       const bool tr = (pair == blockIdx.x);
       const int gofs = g * 5000;
       if (tr && issuer) TBN_TRACE(gofs + 1000 + 4 * j);
@@ -483,7 +489,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
       ptx::tc_fence_after();
-      seg_acquire(false);
+      if (!is_att) seg_acquire(false);
       if (tr && issuer) TBN_TRACE(gofs + 1003 + 4 * j);
     };
     auto nopost = [] {};

@@ -418,8 +418,16 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       for (uint32_t u = 0; u < (uint32_t)CF::NSLOT; ++u) issue_block(u);
     }
     ptx::mbar_wait(&bars->cfull, 0);
-    const float* scale = a.scale ? a.scale : cst + CF::C_SCALE;
-    const float* shift = a.shift ? a.shift : cst + CF::C_SHIFT;
+    if (a.scale) {     // batch-statistics control: override the affine in this CTA's SMEM copy
+      float* cw = reinterpret_cast<float*>(smem + SM::OFF_CONST);
+      for (int f = threadIdx.x; f < F; f += blockDim.x) {
+        cw[CF::C_SCALE + f] = a.scale[f];
+        cw[CF::C_SHIFT + f] = a.shift[f];
+      }
+      ptx::named_bar_sync(13, CF::THREADS);
+    }
+    const float* scale = cst + CF::C_SCALE;
+    const float* shift = cst + CF::C_SHIFT;
     uint32_t xphase = 0, dphase = 0;
 
     // Ping-pong token (FA4 style): the two row groups' CUDA-core segments (the
@@ -486,10 +494,12 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         if (tr && issuer) TBN_TRACE(gofs + 1002 + 4 * j);
       }
       post();
+      // take the token first: while the other group computes, this group's
+      // threads sleep in bar.sync instead of spinning on the mbarrier
+      if (!is_att) seg_acquire(false);
       ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
       ptx::tc_fence_after();
-      if (!is_att) seg_acquire(false);
       if (tr && issuer) TBN_TRACE(gofs + 1003 + 4 * j);
     };
     auto nopost = [] {};
@@ -594,6 +604,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       {
         const int ne = nrows * F;
         const int nbulk = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
+        const bool full_tile = (nbulk == 128 * F);
         if constexpr (!CF::DENSE_IO) {
           claim_ts();
           for (int e = (int)(threadIdx.x % 256); e < 128 * F; e += 256) {
@@ -621,7 +632,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
                 float xv;
                 if constexpr (CF::DENSE_IO) {
                   const int e = t * F + f;
-                  xv = (e < nbulk) ? xs[e] : (e < ne ? __ldg(a.x + r0 * F + e) : 0.0f);
+                  if (full_tile) xv = xs[e];
+                  else xv = (e < nbulk) ? xs[e] : (e < ne ? __ldg(a.x + r0 * F + e) : 0.0f);
                 } else {
                   xv = ts[f * 129 + t];
                 }

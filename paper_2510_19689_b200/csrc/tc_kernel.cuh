@@ -434,12 +434,18 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     // work between two GEMMs) strictly alternate, so each group's tcgen05 MMAs
     // run while the other group computes.  Named barrier 11+g = "group g may
     // run its next segment"; the other group arrives on it when its segment ends.
+    // The token is held only across a segment's TMEM-load phase (released as
+    // soon as the accumulator is in registers, or at the segment's end at the
+    // latest), so one group's TMEM load latency overlaps the other group's math.
     bool paired = false;        // both groups have a tile in the current pair
+    bool token_held = false;
     auto seg_acquire = [&](bool first_of_pair) {
       if (paired && !(g == 0 && first_of_pair)) ptx::named_bar_sync(11 + g, 512);
+      token_held = paired;
     };
     auto seg_release = [&]() {
-      if (paired) ptx::named_bar_arrive(11 + (g ^ 1), 512);
+      if (token_held) ptx::named_bar_arrive(11 + (g ^ 1), 512);
+      token_held = false;
     };
     // A is written (both halves) -> barrier -> one thread issues GEMM j of the
     // tile's sequence -> everyone waits for the accumulator.  `post` runs
@@ -451,7 +457,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       // parity is preserved.
       const bool after_att = (j >= 5) && ((j - 5) % 5 == 0);
       const bool is_att = (j >= 4) && ((j - 4) % 5 == 0);
-      if (!after_att) seg_release();
+      if (!after_att) seg_release();       // no-op if the GLU already released it
       const bool tr = (pair == blockIdx.x);
       const int gofs = g * 5000;
       if (tr && issuer) TBN_TRACE(gofs + 1000 + 4 * j);
@@ -518,6 +524,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         tmem_load_n<CW>(tD + c0 + j0, lin);
         tmem_load_n<CW>(tD + H + c0 + j0, gate);
         ptx::tmem_ld_wait();
+        seg_release();
 #pragma unroll
         for (int i = 0; i < CW; i += 2) {
           const float2 nb = *reinterpret_cast<const float2*>(b + H + c0 + j0 + i);

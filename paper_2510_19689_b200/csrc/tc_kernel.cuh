@@ -79,7 +79,7 @@ struct Cfg {
   static constexpr bool DENSE_IO = (F % 2 == 1) || (F <= 16);
   static constexpr int XSTAGE = rup(128 * F * 4, 128);
   static constexpr int TSTAGE = DENSE_IO ? rup(128 * F * 4, 128) : rup(F * 129 * 4, 128);
-  static constexpr int FIXED = rup(CONST_BYTES, 128) + NG * (XSTAGE + TSTAGE + 4096) + 1024;
+  static constexpr int FIXED = rup(CONST_BYTES, 128) + NG * (XSTAGE + TSTAGE + 8192) + 1024;
   static constexpr int RING_SLOT_ALL = cmax(cmax(B_SH1, B_HID), B_ATT);
   static constexpr int RING_SLOT_RES = cmax(B_HID, B_ATT);
   static constexpr int SMEM_BUDGET = 225 * 1024;
@@ -263,7 +263,7 @@ struct Smem {
   static constexpr int OFF_RES = rup(OFF_T + CF::NG * CF::TSTAGE, 1024);
   static constexpr int OFF_RING = OFF_RES + CF::RES_BYTES;
   static constexpr int OFF_XCH = OFF_RING + CF::NG * CF::NSLOT * CF::SLOT;   // 4 KB per group
-  static constexpr int OFF_BAR = OFF_XCH + CF::NG * 4096;
+  static constexpr int OFF_BAR = OFF_XCH + CF::NG * 8192;   // float4 pair-exchange buffer
   static constexpr int TOTAL = OFF_BAR + 256;
   static_assert(TOTAL <= 227 * 1024, "smem");
 };
@@ -578,15 +578,19 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     };
     // (a, b) exchange with the partner warp of the same lane quarter (the other
     // column half): double-buffered by parity, one 64-thread barrier each.
-    float2* xbuf = reinterpret_cast<float2*>(smem + SM::OFF_XCH) + g * 512;
+    float4* xb4 = reinterpret_cast<float4*>(smem + SM::OFF_XCH) + g * 512;
     const uint32_t pair_bar = 3 + g * 4 + (warp & 3);
     uint32_t xpar = 0;
-    auto xchg = [&](float va, float vb) -> float2 {
-      xbuf[(xpar * 2 + half) * 128 + t] = f2(va, vb);
+    auto xchg4 = [&](float va, float vb, float vc) -> float4 {
+      xb4[(xpar * 2 + half) * 128 + t] = make_float4(va, vb, vc, 0.0f);
       ptx::named_bar_sync(pair_bar, 64);
-      const float2 o = xbuf[(xpar * 2 + (half ^ 1)) * 128 + t];
+      const float4 o = xb4[(xpar * 2 + (half ^ 1)) * 128 + t];
       xpar ^= 1;
       return o;
+    };
+    auto xchg = [&](float va, float vb) -> float2 {
+      const float4 o = xchg4(va, vb, 0.0f);
+      return f2(o.x, o.y);
     };
     auto ts_at = [&](int f) -> float& {
       if constexpr (CF::DENSE_IO) return ts[t * F + f];
@@ -708,69 +712,65 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           constexpr int HB = decltype(hc)::value * KH;             // first feature
           constexpr int FE = (HB + KH < F) ? HB + KH : F;
           constexpr int NF = FE > HB ? FE - HB : 0;               // own features
-          float z[NF > 0 ? NF : 1];
+          constexpr int NFA = NF > 0 ? NF : 1;
+          float z[NFA], pr[NFA], xnv[NFA];
           const float* batt = cst + CF::C_BATT + (s - 1) * CF::FN + HB;
-          float zmax = -INFINITY;
-          chunked<NF>([&](auto o, auto l) {
-            constexpr int O = decltype(o)::value, L = decltype(l)::value;
-            float pr[L];
-            tmem_load_n<L, O>(tD + HB + O, z);
-            tmem_load_n<L>(tPR + HB + O, pr);
+          if constexpr (NF > 0) {                                  // one TMEM round trip
+            tmem_load_n<NF>(tD + HB, z);
+            tmem_load_n<NF>(tPR + HB, pr);
+            tmem_load_n<NF>(tXN + HB, xnv);
             ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < L; ++i) {
-              z[O + i] = pr[i] * (z[O + i] + batt[O + i]);          // network.py:233-235
-              zmax = fmaxf(zmax, z[O + i]);
-            }
-          });
-          zmax = fmaxf(zmax, xchg(zmax, 0.0f).x);
-          float own = 0.0f;
+          }
+          float zmax = -INFINITY, zsum = 0.0f;
 #pragma unroll
           for (int i = 0; i < NF; ++i) {
-            z[i] -= zmax;                                           // sparsemax.py:32
-            own += z[i];
+            z[i] = pr[i] * (z[i] + batt[i]);                        // network.py:233-235
+            zmax = fmaxf(zmax, z[i]);
+            zsum += z[i];
           }
+          {
+            const float2 o = xchg(zmax, zsum);
+            zmax = fmaxf(zmax, o.x);
+            zsum += o.y;
+          }
+#pragma unroll
+          for (int i = 0; i < NF; ++i) z[i] -= zmax;                // sparsemax.py:32
           if (trs) TBN_TRACE(3001 + 8 * s);
           // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
           // monotone from any lower bound of tau*; its support equals the
           // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
-          // max(-1, (sum z - 1)/F): both bound tau* from below.
-          float tau = fmaxf(-1.0f, ((own + xchg(own, 0.0f).x) - 1.0f) * (1.0f / (float)F));
-          // The loop runs warp-uniformly (bar.sync inside must be executed by
-          // whole warps): a converged row keeps its tau until all 32 rows of the
-          // warp — the same rows as the partner warp — have converged.
-          float cnt_prev = (float)(F + 1);
+          // max(-1, (sum z - 1)/F) (the max alone; all elements), nudged down by
+          // 2^-20 relative so rounding cannot push it above tau*.  Converged as
+          // soon as the support's smallest element stays above the new tau (no
+          // element leaves, none can join as tau only grows): no confirmation pass.
+          const float bound = (zsum - (float)F * zmax - 1.0f) * (1.0f / (float)F);
+          float tau = fmaxf(-1.0f, bound - 9.5367431640625e-07f * fmaxf(1.0f, fabsf(bound)));
           bool done = false;
           for (int it = 0; it <= F; ++it) {
-            float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
+            float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f);
+            float mn = INFINITY;
 #pragma unroll
             for (int i = 0; i + 1 < NF; i += 2) {
-              const float2 m = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
-              if ((i / 2) % 2 == 0) {
-                sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
-                ca = __fadd2_rn(ca, m);
-              } else {
-                sb = __ffma2_rn(m, f2(z[i], z[i + 1]), sb);
-                cb = __fadd2_rn(cb, m);
-              }
+              const bool p0 = z[i] > tau, p1 = z[i + 1] > tau;
+              const float2 m = f2(p0 ? 1.0f : 0.0f, p1 ? 1.0f : 0.0f);
+              sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
+              ca = __fadd2_rn(ca, m);
+              mn = fminf(mn, fminf(p0 ? z[i] : INFINITY, p1 ? z[i + 1] : INFINITY));
             }
-            const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
-            float sm = s2.x + s2.y, c = c2.x + c2.y;
+            float sm = sa.x + sa.y, c = ca.x + ca.y;
             if constexpr (NF % 2) {
-              const float m = z[NF - 1] > tau ? 1.0f : 0.0f;
-              sm = fmaf(m, z[NF - 1], sm);
-              c += m;
+              const bool p0 = z[NF - 1] > tau;
+              sm += p0 ? z[NF - 1] : 0.0f;
+              c += p0 ? 1.0f : 0.0f;
+              mn = fminf(mn, p0 ? z[NF - 1] : INFINITY);
             }
-            const float2 o = xchg(sm, c);
+            const float4 o = xchg4(sm, c, mn);
             sm += o.x;
             c += o.y;
+            mn = fminf(mn, o.z);
             if (!done) {
-              if (c >= cnt_prev) {
-                done = true;
-              } else {
-                cnt_prev = c;
-                tau = __fdividef(sm - 1.0f, c);                       // sparsemax.py:39
-              }
+              tau = __fdividef(sm - 1.0f, c);                         // sparsemax.py:39
+              done = mn > tau;
             }
             if (__all_sync(0xffffffffu, done)) break;
           }
@@ -783,25 +783,21 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
             constexpr int O = decltype(o)::value, L = decltype(l)::value;
             constexpr int FB = HB + O;
             constexpr int LF = (FB + L <= F) ? L : (FB < F ? F - FB : 0);
-            float pr[L], xnv[L], xm[L];
-            if constexpr (LF > 0) {
-              tmem_load_n<LF>(tPR + FB, pr);
-              tmem_load_n<LF>(tXN + FB, xnv);
-              ptx::tmem_ld_wait();
-            }
+            float prn[L], xm[L];
 #pragma unroll
             for (int i = 0; i < L; ++i) {
               const int f = FB + i;
               if (f < F) {
                 const float m = fmaxf(z[O + i] - tau, 0.0f);          // sparsemax.py:40
-                pr[i] = pr[i] * (p.gamma - m);                        // network.py:237
-                xm[i] = m * xnv[i];                                   // network.py:238
+                prn[i] = pr[O + i] * (p.gamma - m);                   // network.py:237
+                xm[i] = m * xnv[O + i];                               // network.py:238
                 ts_at(f) = m;
               } else {
+                prn[i] = 0.0f;
                 xm[i] = 0.0f;
               }
             }
-            if constexpr (LF > 0) tmem_store_n<LF>(tPR + FB, pr);
+            if constexpr (LF > 0) tmem_store_n<LF>(tPR + FB, prn);
             store_a<CF, L>(tA + FB, tAL + FB, xm);
           });
           if (trs) TBN_TRACE(3004 + 8 * s);

@@ -740,37 +740,42 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           // monotone from any lower bound of tau*; its support equals the
           // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
           // max(-1, (sum z - 1)/F) (the max alone; all elements), nudged down by
-          // 2^-20 relative so rounding cannot push it above tau*.  Converged as
-          // soon as the support's smallest element stays above the new tau (no
-          // element leaves, none can join as tau only grows): no confirmation pass.
+          // 2^-20 relative so rounding cannot push it above tau*.  The loop runs
+          // warp-uniformly (bar.sync inside); a converged row keeps its tau.
           const float bound = (zsum - (float)F * zmax - 1.0f) * (1.0f / (float)F);
           float tau = fmaxf(-1.0f, bound - 9.5367431640625e-07f * fmaxf(1.0f, fabsf(bound)));
+          float cnt_prev = (float)(F + 1);
           bool done = false;
           for (int it = 0; it <= F; ++it) {
-            float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f);
-            float mn = INFINITY;
+            float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
 #pragma unroll
             for (int i = 0; i + 1 < NF; i += 2) {
-              const bool p0 = z[i] > tau, p1 = z[i + 1] > tau;
-              const float2 m = f2(p0 ? 1.0f : 0.0f, p1 ? 1.0f : 0.0f);
-              sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
-              ca = __fadd2_rn(ca, m);
-              mn = fminf(mn, fminf(p0 ? z[i] : INFINITY, p1 ? z[i + 1] : INFINITY));
+              const float2 m = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
+              if ((i / 2) % 2 == 0) {
+                sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
+                ca = __fadd2_rn(ca, m);
+              } else {
+                sb = __ffma2_rn(m, f2(z[i], z[i + 1]), sb);
+                cb = __fadd2_rn(cb, m);
+              }
             }
-            float sm = sa.x + sa.y, c = ca.x + ca.y;
+            const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
+            float sm = s2.x + s2.y, c = c2.x + c2.y;
             if constexpr (NF % 2) {
-              const bool p0 = z[NF - 1] > tau;
-              sm += p0 ? z[NF - 1] : 0.0f;
-              c += p0 ? 1.0f : 0.0f;
-              mn = fminf(mn, p0 ? z[NF - 1] : INFINITY);
+              const float m = z[NF - 1] > tau ? 1.0f : 0.0f;
+              sm = fmaf(m, z[NF - 1], sm);
+              c += m;
             }
-            const float4 o = xchg4(sm, c, mn);
+            const float2 o = xchg(sm, c);
             sm += o.x;
             c += o.y;
-            mn = fminf(mn, o.z);
             if (!done) {
-              tau = __fdividef(sm - 1.0f, c);                         // sparsemax.py:39
-              done = mn > tau;
+              if (c >= cnt_prev) {
+                done = true;
+              } else {
+                cnt_prev = c;
+                tau = __fdividef(sm - 1.0f, c);                       // sparsemax.py:39
+              }
             }
             if (__all_sync(0xffffffffu, done)) break;
           }

@@ -27,13 +27,15 @@ float tf32_rna_host(float x) {
 // blocks: float index (n/8)*(Kp*8) + (k/4)*32 + (n%8)*4 + (k%4).  Rows n >= Nvalid
 // and columns k >= Kin are zero.
 void pack_block(std::vector<float>& img, size_t off_floats, const double* W, int Kin, int Nvalid,
-                int N, int Kp, bool x3, int col_stride, const std::vector<double>* colscale = nullptr) {
+                int N, int Kp, bool x3, int col_stride, const std::vector<double>* colscale = nullptr,
+                const double* bias = nullptr) {
   float* hi = img.data() + off_floats;
   float* lo = hi + (size_t)N * Kp;
   for (int n = 0; n < N; ++n)
     for (int k = 0; k < Kp; ++k) {
       const size_t idx = (size_t)(n / 8) * (Kp * 8) + (k / 4) * 32 + (n % 8) * 4 + (k % 4);
       double w = (n < Nvalid && k < Kin) ? W[(size_t)k * col_stride + n] : 0.0;
+      if (bias && n < Nvalid && k == Kin) w = bias[n];     // bias row (ones column in A)
       if (colscale) w *= (*colscale)[n];
       float h = tf32_rna_host((float)w);
       hi[idx] = h;
@@ -91,15 +93,17 @@ bool pack_impl(const HostParams& hp, TcModel* out, std::string* err) {
   const size_t bytes = off;
   std::vector<float> img(bytes / 4, 0.0f);
   std::memcpy(img.data(), c.data(), c.size() * 4);
-  pack_block(img, tp.off_sh1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first);
-  pack_block(img, tp.off_sh2 / 4, hp.sh2_W, H, N2, N2, H, CF::X3, N2, &cs_res);
+  pack_block(img, tp.off_sh1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first, hp.sh1_b);
+  pack_block(img, tp.off_sh2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, CF::X3, N2, &cs_res, hp.sh2_b);
   for (int s = 0; s <= S; ++s) {
-    pack_block(img, (tp.off_fc1 + (size_t)s * CF::B_HID) / 4, hp.fc1_W[s], H, N2, N2, H, CF::X3, N2, &cs_res);
-    pack_block(img, (tp.off_fc2 + (size_t)s * CF::B_HID) / 4, hp.fc2_W[s], H, N2, N2, H, CF::X3, N2, &cs_res);
+    pack_block(img, (tp.off_fc1 + (size_t)s * CF::B_HID) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, CF::X3, N2,
+               &cs_res, hp.fc1_b[s]);
+    pack_block(img, (tp.off_fc2 + (size_t)s * CF::B_HID) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, CF::X3, N2,
+               &cs_res, hp.fc2_b[s]);
   }
   for (int s = 1; s <= S; ++s)
-    pack_block(img, (tp.off_att + (size_t)(s - 1) * CF::B_ATT) / 4, hp.att_W[s], NA, F, CF::FN, NA,
-               CF::X3, F);
+    pack_block(img, (tp.off_att + (size_t)(s - 1) * CF::B_ATT) / 4, hp.att_W[s], NA, F, CF::FN, CF::KATT,
+               CF::X3, F, nullptr, hp.att_b[s]);
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), bytes, cudaMemcpyHostToDevice);

@@ -48,9 +48,13 @@ struct Cfg {
   static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
   static constexpr int H = ND + NA, N2 = 2 * H;
   static constexpr bool X3 = (PREC == kPrecTF32x3);
-  static constexpr int K1 = rup(F, 8);                 // shared1 K (tf32 granule 8)
+  // Every GEMM carries its bias as an extra K row of B, multiplied by a column
+  // of ones in A at index F (shared1), H (hidden) or NA (attentive).
+  static constexpr int K1 = rup(F + 1, 8);             // shared1 K (tf32 granule 8)
+  static constexpr int KHID = H + 8;                   // shared2 / fc1 / fc2 K
+  static constexpr int KATT = NA + 8;                  // attentive K
   static constexpr int FN = rup(F, 16);                // attentive N (M=128 needs N%16==0)
-  static constexpr int KA = cmax(cmax(K1, H), NA);     // A operand columns
+  static constexpr int KA = cmax(cmax(K1, KHID), KATT); // A operand columns
   static constexpr int DW = cmax(N2, FN);              // accumulator columns
   // TMEM column map (per group)
   static constexpr int T_D = 0, T_A = DW, T_AL = T_A + KA, T_XN = T_AL + (X3 ? KA : 0);
@@ -63,8 +67,8 @@ struct Cfg {
   // weight blocks (B operands, K-major canonical, hi [+ lo])
   static constexpr int PARTS = X3 ? 2 : 1;
   static constexpr int B_SH1 = PARTS * N2 * K1 * 4;
-  static constexpr int B_HID = PARTS * N2 * H * 4;     // shared2, fc1_s, fc2_s
-  static constexpr int B_ATT = PARTS * FN * NA * 4;
+  static constexpr int B_HID = PARTS * N2 * KHID * 4;  // shared2, fc1_s, fc2_s
+  static constexpr int B_ATT = PARTS * FN * KATT * 4;
   // consts (floats): scale F | shift F | bias sh1 N2 | sh2 N2 | fc1 (S+1)N2 | fc2 (S+1)N2 |
   //                  att S*FN | head_W ND*C | head_b C
   static constexpr int C_SCALE = 0, C_SHIFT = C_SCALE + rup(F, 4), C_BSH1 = C_SHIFT + rup(F, 4);
@@ -494,8 +498,8 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           bsm = ptx::smem_u32(ring + (u % CF::NSLOT) * CF::SLOT);
         }
         if (kind == 0) issue_gemm<CF, K1, CF::N2>(tD, tA, tAL, bsm);
-        else if (kind == 4) issue_gemm<CF, NA, CF::FN>(tD, tA, tAL, bsm);
-        else issue_gemm<CF, H, CF::N2>(tD, tA, tAL, bsm);
+        else if (kind == 4) issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tAL, bsm);
+        else issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tAL, bsm);
         ptx::mma_commit(&bars->dfull[g]);
         if (tr && issuer) TBN_TRACE(gofs + 1002 + 4 * j);
       }
@@ -515,7 +519,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     // blocks' linear columns carry sqrt(.5); b = [b_lin' (H) | -log2e*b_gate (H)].
     //   e = 2^(gate'+nb) = exp(-u_gate);  sigma = 1/(1+e)  (one rcp per pair:
     //   q = 1/(d0 d1), sigma0 = d1 q, sigma1 = d0 q);  out = (lin'+b')*sigma [+ sqrt(.5)*prev]
-    auto glu = [&](const float* b, bool residual, float (&prev)[HH]) {
+    auto glu = [&](bool residual, float (&prev)[HH]) {
       constexpr int CW = HH < 32 ? HH : 32;
       const int c0 = half * HH;
 #pragma unroll
@@ -527,25 +531,29 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         seg_release();
 #pragma unroll
         for (int i = 0; i < CW; i += 2) {
-          const float2 nb = *reinterpret_cast<const float2*>(b + H + c0 + j0 + i);
-          const float2 bl = *reinterpret_cast<const float2*>(b + c0 + j0 + i);
-          float2 arg = __fadd2_rn(f2(gate[i], gate[i + 1]), nb);
-          arg.x = fminf(arg.x, 63.0f);       // keep d0*d1 finite (sigma < 2^-63 there)
-          arg.y = fminf(arg.y, 63.0f);
-          const float2 d = __fadd2_rn(f2(ex2_approx(arg.x), ex2_approx(arg.y)), f2(1.0f, 1.0f));
+          // D already holds lin' + b' and gate' + b' (bias row in B, ones in A)
+          const float a0 = fminf(gate[i], 63.0f), a1 = fminf(gate[i + 1], 63.0f);
+          const float2 d = __fadd2_rn(f2(ex2_approx(a0), ex2_approx(a1)), f2(1.0f, 1.0f));
           const float q = rcp_approx(d.x * d.y);
           const float2 sg = __fmul2_rn(f2(d.y, d.x), f2(q, q));
-          const float2 l = __fadd2_rn(f2(lin[i], lin[i + 1]), bl);
           float2 o;
           if (residual) {
             const float2 rp = __fmul2_rn(f2(prev[j0 + i], prev[j0 + i + 1]), f2(kR, kR));
-            o = __ffma2_rn(l, sg, rp);
+            o = __ffma2_rn(f2(lin[i], lin[i + 1]), sg, rp);
           } else {
-            o = __fmul2_rn(l, sg);
+            o = __fmul2_rn(f2(lin[i], lin[i + 1]), sg);
           }
           prev[j0 + i] = o.x;
           prev[j0 + i + 1] = o.y;
         }
+      }
+    };
+    // ones column of the hidden GEMMs' A (cols [H, H+8) = 1,0,..,0), rewritten
+    // after each shared1 GEMM (whose A used those columns for features/ones)
+    auto store_hidden_ones = [&]() {
+      if (half == 1) {
+        float v[8] = {1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+        store_a<CF, 8>(tA + H, tAL + H, v);
       }
     };
     auto store_half = [&](const float (&v)[HH]) {     // A columns [half*H/2, +H/2)
@@ -651,7 +659,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
                 bad |= !isfinite(xv);
                 xn[i] = a.normalized ? xv : (xv - shift[f]) * scale[f];
               } else {
-                xn[i] = 0.0f;
+                xn[i] = (f == F) ? 1.0f : 0.0f;                       // ones column (bias row)
               }
             }
             if constexpr (LF > 0) {
@@ -684,22 +692,28 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       // feature transformer (network.py:124-141): 4 GEMM+GLU blocks
       auto transform = [&](int step, auto&& post_first) {
         gemm(j++, pair, post_first);
-        glu(cst + CF::C_BSH1, false, prev);                          // g1 = GLU(u1)
+        glu(false, prev);                                            // g1 = GLU(u1)
+        store_half(prev);
+        store_hidden_ones();
+        gemm(j++, pair, nopost);
+        glu(true, prev);                                             // g2
         store_half(prev);
         gemm(j++, pair, nopost);
-        glu(cst + CF::C_BSH2, true, prev);                           // g2
+        glu(true, prev);                                             // g3
         store_half(prev);
         gemm(j++, pair, nopost);
-        glu(cst + CF::C_BFC1 + step * CF::N2, true, prev);           // g3
-        store_half(prev);
-        gemm(j++, pair, nopost);
-        glu(cst + CF::C_BFC2 + step * CF::N2, true, prev);           // g4 = f
+        glu(true, prev);                                             // g4 = f
       };
 
       transform(0, nopost);                                           // network.py:226-227
       for (int s = 1; s <= S; ++s) {
         // A <- a = f[:, n_d:]  (half 1 owns it)
-        if (half == 1) store_a_all<CF, NA>(tA, tAL, prev);
+        if (half == 1) {
+          float av[CF::KATT];
+#pragma unroll
+          for (int k = 0; k < CF::KATT; ++k) av[k] = k < NA ? prev[k] : (k == NA ? 1.0f : 0.0f);
+          store_a_all<CF, CF::KATT>(tA, tAL, av);
+        }
         gemm(j++, pair, nopost);
         const bool trs = (g == 0 && pair == blockIdx.x && issuer);
         if (trs) TBN_TRACE(3000 + 8 * s);
@@ -714,7 +728,6 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           constexpr int NF = FE > HB ? FE - HB : 0;               // own features
           constexpr int NFA = NF > 0 ? NF : 1;
           float z[NFA], pr[NFA], xnv[NFA];
-          const float* batt = cst + CF::C_BATT + (s - 1) * CF::FN + HB;
           if constexpr (NF > 0) {                                  // one TMEM round trip
             tmem_load_n<NF>(tD + HB, z);
             tmem_load_n<NF>(tPR + HB, pr);
@@ -724,7 +737,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           float zmax = -INFINITY, zsum = 0.0f;
 #pragma unroll
           for (int i = 0; i < NF; ++i) {
-            z[i] = pr[i] * (z[i] + batt[i]);                        // network.py:233-235
+            z[i] = pr[i] * z[i];                                    // network.py:233-235 (bias in D)
             zmax = fmaxf(zmax, z[i]);
             zsum += z[i];
           }
@@ -799,7 +812,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
                 ts_at(f) = m;
               } else {
                 prn[i] = 0.0f;
-                xm[i] = 0.0f;
+                xm[i] = (f == F) ? 1.0f : 0.0f;                       // ones column (bias row)
               }
             }
             if constexpr (LF > 0) tmem_store_n<LF>(tPR + FB, prn);

@@ -507,8 +507,10 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       // take the token first: while the other group computes, this group's
       // threads sleep in bar.sync instead of spinning on the mbarrier
       if (!is_att) seg_acquire(false);
-      ptx::mbar_wait(&bars->dfull[g], dphase);
+      // one warp polls the accumulator barrier; the rest sleep in bar.sync
+      if ((warp & 7) == 0) ptx::mbar_wait(&bars->dfull[g], dphase);
       dphase ^= 1;
+      ptx::named_bar_sync(bar_id, 256);
       ptx::tc_fence_after();
       if (tr && issuer) TBN_TRACE(gofs + 1003 + 4 * j);
     };

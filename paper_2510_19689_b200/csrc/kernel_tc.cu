@@ -23,12 +23,39 @@ float tf32_rna_host(float x) {
   return y;
 }
 
+uint16_t bf16_rn_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);       // round to nearest even (finite inputs)
+  return (uint16_t)(u >> 16);
+}
+
+// bf16 variant: 16-bit elements, 8 per 16-byte core-matrix row:
+// element index (n/8)*(Kp*8) + (k/8)*64 + (n%8)*8 + (k%8).
+void pack_block_bf16(std::vector<float>& img, size_t off_floats, const double* W, int Kin, int Nvalid,
+                     int N, int Kp, int col_stride, const std::vector<double>* colscale,
+                     const double* bias) {
+  uint16_t* b = reinterpret_cast<uint16_t*>(img.data() + off_floats);
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < Kp; ++k) {
+      const size_t idx = (size_t)(n / 8) * (Kp * 8) + (k / 8) * 64 + (n % 8) * 8 + (k % 8);
+      double w = (n < Nvalid && k < Kin) ? W[(size_t)k * col_stride + n] : 0.0;
+      if (bias && n < Nvalid && k == Kin) w = bias[n];
+      if (colscale) w *= (*colscale)[n];
+      b[idx] = bf16_rn_host((float)w);
+    }
+}
+
 // Pack W (Kin x N, row-major, x @ W) into B = W^T as N x Kp K-major canonical
 // blocks: float index (n/8)*(Kp*8) + (k/4)*32 + (n%8)*4 + (k%4).  Rows n >= Nvalid
 // and columns k >= Kin are zero.
 void pack_block(std::vector<float>& img, size_t off_floats, const double* W, int Kin, int Nvalid,
                 int N, int Kp, bool x3, int col_stride, const std::vector<double>* colscale = nullptr,
-                const double* bias = nullptr) {
+                const double* bias = nullptr, bool bf16 = false) {
+  if (bf16) {
+    pack_block_bf16(img, off_floats, W, Kin, Nvalid, N, Kp, col_stride, colscale, bias);
+    return;
+  }
   float* hi = img.data() + off_floats;
   float* lo = hi + (size_t)N * Kp;
   for (int n = 0; n < N; ++n)
@@ -93,17 +120,17 @@ bool pack_impl(const HostParams& hp, TcModel* out, std::string* err) {
   const size_t bytes = off;
   std::vector<float> img(bytes / 4, 0.0f);
   std::memcpy(img.data(), c.data(), c.size() * 4);
-  pack_block(img, tp.off_sh1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first, hp.sh1_b);
-  pack_block(img, tp.off_sh2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, CF::X3, N2, &cs_res, hp.sh2_b);
+  pack_block(img, tp.off_sh1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first, hp.sh1_b, CF::BF);
+  pack_block(img, tp.off_sh2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, CF::X3, N2, &cs_res, hp.sh2_b, CF::BF);
   for (int s = 0; s <= S; ++s) {
     pack_block(img, (tp.off_fc1 + (size_t)s * CF::B_HID) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, CF::X3, N2,
-               &cs_res, hp.fc1_b[s]);
+               &cs_res, hp.fc1_b[s], CF::BF);
     pack_block(img, (tp.off_fc2 + (size_t)s * CF::B_HID) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, CF::X3, N2,
-               &cs_res, hp.fc2_b[s]);
+               &cs_res, hp.fc2_b[s], CF::BF);
   }
   for (int s = 1; s <= S; ++s)
     pack_block(img, (tp.off_att + (size_t)(s - 1) * CF::B_ATT) / 4, hp.att_W[s], NA, F, CF::FN, CF::KATT,
-               CF::X3, F, nullptr, hp.att_b[s]);
+               CF::X3, F, nullptr, hp.att_b[s], CF::BF);
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), bytes, cudaMemcpyHostToDevice);
@@ -143,14 +170,19 @@ cudaError_t launch_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cud
 const Instance kInstances[] = {
     TBN_INSTANCE(14, 8, 8, 3, 2, tc::kPrecTF32x3),   // Adult
     TBN_INSTANCE(14, 8, 8, 3, 2, tc::kPrecTF32),
+    TBN_INSTANCE(14, 8, 8, 3, 2, tc::kPrecBF16),
     TBN_INSTANCE(35, 16, 16, 5, 2, tc::kPrecTF32x3), // HR
     TBN_INSTANCE(35, 16, 16, 5, 2, tc::kPrecTF32),
+    TBN_INSTANCE(35, 16, 16, 5, 2, tc::kPrecBF16),
     TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecTF32x3), // BLS
     TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecTF32),
+    TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecBF16),
 };
 
 const Instance* find(const HostParams& hp, int precision) {
-  int prec = precision == 0 ? tc::kPrecTF32x3 : (precision == 1 ? tc::kPrecTF32 : -1);
+  int prec = precision == 0 ? tc::kPrecTF32x3
+             : precision == 1 ? tc::kPrecTF32
+             : precision == 2 ? tc::kPrecBF16 : -1;
   for (const Instance& in : kInstances)
     if (in.F == hp.F && in.ND == hp.ND && in.NA == hp.NA && in.S == hp.S && in.C == hp.C && in.prec == prec)
       return &in;

@@ -26,6 +26,7 @@
 #pragma once
 #include <cstdint>
 #include <type_traits>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include "tc_ptx.cuh"
 #include "tbn_internal.h"
@@ -35,6 +36,7 @@ namespace tc {
 
 constexpr int kPrecTF32x3 = 0;
 constexpr int kPrecTF32 = 1;
+constexpr int kPrecBF16 = 2;
 
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
@@ -48,13 +50,17 @@ struct Cfg {
   static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
   static constexpr int H = ND + NA, N2 = 2 * H;
   static constexpr bool X3 = (PREC == kPrecTF32x3);
+  static constexpr bool BF = (PREC == kPrecBF16);    // kind::f16 with bf16 operands
+  static constexpr int KG = BF ? 16 : 8;             // MMA K granule
+  static constexpr int ESZ = BF ? 2 : 4;             // operand element bytes
   // Every GEMM carries its bias as an extra K row of B, multiplied by a column
   // of ones in A at index F (shared1), H (hidden) or NA (attentive).
-  static constexpr int K1 = rup(F + 1, 8);             // shared1 K (tf32 granule 8)
-  static constexpr int KHID = H + 8;                   // shared2 / fc1 / fc2 K
-  static constexpr int KATT = NA + 8;                  // attentive K
+  static constexpr int K1 = rup(F + 1, KG);            // shared1 K
+  static constexpr int KHID = H + KG;                  // shared2 / fc1 / fc2 K
+  static constexpr int KATT = NA + KG;                 // attentive K
   static constexpr int FN = rup(F, 16);                // attentive N (M=128 needs N%16==0)
-  static constexpr int KA = cmax(cmax(K1, KHID), KATT); // A operand columns
+  static constexpr int KA_EL = cmax(cmax(K1, KHID), KATT); // A operand elements
+  static constexpr int KA = BF ? KA_EL / 2 : KA_EL;          // A operand TMEM columns
   static constexpr int DW = cmax(N2, FN);              // accumulator columns
   // TMEM column map (per group)
   static constexpr int T_D = 0, T_A = DW, T_AL = T_A + KA, T_XN = T_AL + (X3 ? KA : 0);
@@ -66,9 +72,9 @@ struct Cfg {
   static_assert(N2 <= 256 && FN <= 256, "MMA N > 256");
   // weight blocks (B operands, K-major canonical, hi [+ lo])
   static constexpr int PARTS = X3 ? 2 : 1;
-  static constexpr int B_SH1 = PARTS * N2 * K1 * 4;
-  static constexpr int B_HID = PARTS * N2 * KHID * 4;  // shared2, fc1_s, fc2_s
-  static constexpr int B_ATT = PARTS * FN * KATT * 4;
+  static constexpr int B_SH1 = PARTS * N2 * K1 * ESZ;
+  static constexpr int B_HID = PARTS * N2 * KHID * ESZ;  // shared2, fc1_s, fc2_s
+  static constexpr int B_ATT = PARTS * FN * KATT * ESZ;
   // consts (floats): scale F | shift F | bias sh1 N2 | sh2 N2 | fc1 (S+1)N2 | fc2 (S+1)N2 |
   //                  att S*FN | head_W ND*C | head_b C
   static constexpr int C_SCALE = 0, C_SHIFT = C_SCALE + rup(F, 4), C_BSH1 = C_SHIFT + rup(F, 4);
@@ -102,7 +108,8 @@ struct Cfg {
   static constexpr int HH = H / 2;                      // GLU columns per half
   static constexpr int KH = K1 / 2;                     // shared1 K columns per half
   static_assert(ND == NA, "column split assumes n_d == n_a (all BASELINE configs)");
-  static_assert(K1 % 8 == 0 && HH % 4 == 0, "half split granularity");
+  static_assert(!BF || (KH % 2 == 0 && HH % 2 == 0), "bf16 A chunks pack element pairs");
+  static_assert(HH % 4 == 0, "half split granularity");
   static constexpr int THREADS = NG * 256;
 };
 
@@ -211,6 +218,17 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 // leaving a 2^-22 relative error per product).
 template <class CF, int L, int M>
 __device__ __forceinline__ void store_a(uint32_t t_a, uint32_t t_al, const float (&v)[M]) {
+  if constexpr (CF::BF) {
+    static_assert(L % 2 == 0, "bf16 A chunks pack element pairs");
+    float pk[L / 2];
+#pragma unroll
+    for (int i = 0; i < L / 2; ++i) {
+      const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);   // low = even
+      pk[i] = *reinterpret_cast<const float*>(&b);
+    }
+    tmem_store_n<L / 2>(t_a, pk);
+    return;
+  }
   tmem_store_n<L>(t_a, v);
   if constexpr (CF::X3) {
     float lo[L];
@@ -227,6 +245,10 @@ __device__ __forceinline__ void store_a(uint32_t t_a, uint32_t t_al, const float
     tmem_store_n<L>(t_al, lo);
   }
 }
+// TMEM column of A element e (bf16 packs two elements per column)
+template <class CF>
+__host__ __device__ constexpr uint32_t acol(int e) { return CF::BF ? (uint32_t)(e / 2) : (uint32_t)e; }
+
 // A <- v[0..K) in 16-column chunks
 template <class CF, int K, int M>
 __device__ __forceinline__ void store_a_all(uint32_t t_a, uint32_t t_al, const float (&v)[M]) {
@@ -235,7 +257,7 @@ __device__ __forceinline__ void store_a_all(uint32_t t_a, uint32_t t_al, const f
     float c[L];
 #pragma unroll
     for (int i = 0; i < L; ++i) c[i] = v[O + i];
-    store_a<CF, L>(t_a + O, t_al + O, c);
+    store_a<CF, L>(t_a + acol<CF>(O), t_al + acol<CF>(O), c);
   });
 }
 
@@ -243,6 +265,15 @@ __device__ __forceinline__ void store_a_all(uint32_t t_a, uint32_t t_al, const f
 // N x K K-major canonical); 3xTF32 adds A_lo x B_hi and A_hi x B_lo.
 template <class CF, int K, int N>
 __device__ __forceinline__ void issue_gemm(uint32_t tD, uint32_t tA, uint32_t tAL, uint32_t bsm) {
+  if constexpr (CF::BF) {
+    constexpr uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtBF16, 128, N);
+    constexpr uint32_t sbo = (K / 8) * 128u;
+    const uint64_t d0 = ptx::smem_desc(bsm, 128u, sbo);
+#pragma unroll
+    for (int k0 = 0; k0 < K; k0 += 16)       // 16 K elements = 2 core matrices = 32 B
+      ptx::mma_f16_ts(tD, tA + k0 / 2, d0 + (uint64_t)k0, idesc, k0 > 0 ? 1u : 0u);
+    return;
+  }
   constexpr uint32_t idesc = ptx::idesc_f32acc(ptx::kFmtTF32, 128, N);
   constexpr uint32_t sbo = (K / 4) * 128u;
   constexpr uint64_t lo = (uint64_t)((N * K * 4) >> 4);     // hi -> lo block, in 16 B units
@@ -554,12 +585,14 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
     // after each shared1 GEMM (whose A used those columns for features/ones)
     auto store_hidden_ones = [&]() {
       if (half == 1) {
-        float v[8] = {1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-        store_a<CF, 8>(tA + H, tAL + H, v);
+        float v[CF::KG];
+#pragma unroll
+        for (int i = 0; i < CF::KG; ++i) v[i] = i == 0 ? 1.0f : 0.0f;
+        store_a<CF, CF::KG>(tA + acol<CF>(H), tAL + acol<CF>(H), v);
       }
     };
-    auto store_half = [&](const float (&v)[HH]) {     // A columns [half*H/2, +H/2)
-      store_a_all<CF, HH>(tA + half * HH, tAL + half * HH, v);
+    auto store_half = [&](const float (&v)[HH]) {     // A elements [half*H/2, +H/2)
+      store_a_all<CF, HH>(tA + acol<CF>(half * HH), tAL + acol<CF>(half * HH), v);
     };
     // Row staging -> global: dense mode = TMA bulk store (+ coalesced tail),
     // transpose mode = cooperative coalesced stores.  Call after a group barrier.
@@ -668,7 +701,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
               tmem_store_n<LF>(tXN + FB, xn);
               tmem_store_n<LF>(tPR + FB, one);
             }
-            store_a<CF, L>(tA + FB, tAL + FB, xn);
+            store_a<CF, L>(tA + acol<CF>(FB), tAL + acol<CF>(FB), xn);
           });
         };
         if (half == 0) {
@@ -818,7 +851,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
               }
             }
             if constexpr (LF > 0) tmem_store_n<LF>(tPR + FB, prn);
-            store_a<CF, L>(tA + FB, tAL + FB, xm);
+            store_a<CF, L>(tA + acol<CF>(FB), tAL + acol<CF>(FB), xm);
           });
           if (trs) TBN_TRACE(3004 + 8 * s);
         };

@@ -4,7 +4,7 @@ import paper_2510_19689_b200 as P
 from paper_2510_19689_b200 import workloads as W
 from oracle import tabnet_oracle as O
 for name in ("adult", "hr", "bls"):
-    for prec in ("tf32x3", "tf32"):
+    for prec in ("tf32x3", "tf32", "bf16"):
         m = P.TabNetModel.from_reference(W.make_model(name, "trained"), precision=prec)
         x = W.make_inputs(W.WORKLOADS[name], 1000).astype(np.float64)
         t0 = time.time()

@@ -740,6 +740,38 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         glu(true, prev);                                             // g4 = f
       };
 
+      // d = relu(f[:, :n_d]); d_sum += d; eta = sum(d); agg += eta*m
+      // (network.py:241-245) for the step just finished (half 0 owns d, agg).
+      // Runs in the next attentive GEMM's shadow (its post hook).
+      bool agg_pending = false;
+      auto agg_update = [&]() {
+        if (!agg_pending) return;
+        agg_pending = false;
+        if (half != 0) return;
+        float eta = 0.0f;
+#pragma unroll
+        for (int i = 0; i < HH; ++i) {
+          const float d = fmaxf(prev[i], 0.0f);
+          dsum[i] += d;
+          eta += d;
+        }
+        // While every eta so far is 0, agg holds sum_s m instead (needed only for
+        // the importance fallback, network.py:259-261, which fires exactly then);
+        // the first eta > 0 resets it to eta*m, identical to the reference's sum.
+        const bool reset = all_eta_zero && eta > 0.0f;
+        const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
+        all_eta_zero = all_eta_zero && !(eta > 0.0f);
+        chunked<F>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          float ag[L];
+          tmem_load_n<L>(tAG + O, ag);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < L; ++i) ag[i] = fmaf(w, ts_at(O + i), reset ? 0.0f : ag[i]);
+          tmem_store_n<L>(tAG + O, ag);
+        });
+      };
+
       transform(0, nopost);                                           // network.py:226-227
       for (int s = 1; s <= S; ++s) {
         // A <- a = f[:, n_d:]  (half 1 owns it)
@@ -749,7 +781,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           for (int k = 0; k < CF::KATT; ++k) av[k] = k < NA ? prev[k] : (k == NA ? 1.0f : 0.0f);
           store_a_all<CF, CF::KATT>(tA, tAL, av);
         }
-        gemm(j++, pair, nopost);
+        gemm(j++, pair, agg_update);        // previous step's eta/agg under the att MMA
         const bool trs = (g == 0 && pair == blockIdx.x && issuer);
         if (trs) TBN_TRACE(3000 + 8 * s);
         // attentive FC + prior + sparsemax (network.py:233-236, sparsemax.py:13-41),
@@ -758,91 +790,93 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         // barrier per exchange).  a+b == b+a in IEEE, so both halves hold
         // bitwise-identical combined values and take identical decisions.
         auto attentive = [&](auto hc) {
-          constexpr int HB = decltype(hc)::value * KH;             // first feature
+          constexpr int HV = decltype(hc)::value;
+          constexpr int HB = HV * KH;                              // first own feature
           constexpr int FE = (HB + KH < F) ? HB + KH : F;
           constexpr int NF = FE > HB ? FE - HB : 0;               // own features
           constexpr int NFA = NF > 0 ? NF : 1;
-          float z[NFA], pr[NFA], xnv[NFA];
-          if constexpr (NF > 0) {                                  // one TMEM round trip
-            tmem_load_n<NF>(tD + HB, z);
-            tmem_load_n<NF>(tPR + HB, pr);
-            tmem_load_n<NF>(tXN + HB, xnv);
+          // half 0 holds the whole row's z (it runs the tau search alone);
+          // half 1 only its own features.
+          constexpr int NZ = HV == 0 ? F : NF;
+          constexpr int ZB = HV == 0 ? 0 : HB;                      // z[i] <-> feature ZB + i
+          float z[NZ > 0 ? NZ : 1], pr[NZ > 0 ? NZ : 1], xnv[NFA];
+          if constexpr (NZ > 0) {
+            tmem_load_n<NZ>(tD + ZB, z);
+            tmem_load_n<NZ>(tPR + ZB, pr);
             ptx::tmem_ld_wait();
           }
-          float zmax = -INFINITY, zsum = 0.0f;
 #pragma unroll
-          for (int i = 0; i < NF; ++i) {
-            z[i] = pr[i] * z[i];                                    // network.py:233-235 (bias in D)
-            zmax = fmaxf(zmax, z[i]);
-            zsum += z[i];
-          }
-          {
-            const float2 o = xchg(zmax, zsum);
-            zmax = fmaxf(zmax, o.x);
-            zsum += o.y;
-          }
+          for (int i = 0; i < NZ; ++i) z[i] = pr[i] * z[i];         // network.py:233-235 (bias in D)
+          if constexpr (NF > 0) tmem_load_n<NF>(tXN + HB, xnv);     // lands during the search
+          float zmax = -INFINITY, tau = 0.0f;
+          if constexpr (HV == 0) {
+            float zsum = 0.0f;
 #pragma unroll
-          for (int i = 0; i < NF; ++i) z[i] -= zmax;                // sparsemax.py:32
-          if (trs) TBN_TRACE(3001 + 8 * s);
-          // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
-          // monotone from any lower bound of tau*; its support equals the
-          // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
-          // max(-1, (sum z - 1)/F) (the max alone; all elements), nudged down by
-          // 2^-20 relative so rounding cannot push it above tau*.  The loop runs
-          // warp-uniformly (bar.sync inside); a converged row keeps its tau.
-          const float bound = (zsum - (float)F * zmax - 1.0f) * (1.0f / (float)F);
-          float tau = fmaxf(-1.0f, bound - 9.5367431640625e-07f * fmaxf(1.0f, fabsf(bound)));
-          float cnt_prev = (float)(F + 1);
-          bool done = false;
-          for (int it = 0; it <= F; ++it) {
-            float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
+            for (int i = 0; i < F; ++i) {
+              zmax = fmaxf(zmax, z[i]);
+              zsum += z[i];
+            }
 #pragma unroll
-            for (int i = 0; i + 1 < NF; i += 2) {
-              const float2 m = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
-              if ((i / 2) % 2 == 0) {
-                sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
-                ca = __fadd2_rn(ca, m);
-              } else {
-                sb = __ffma2_rn(m, f2(z[i], z[i + 1]), sb);
-                cb = __fadd2_rn(cb, m);
+            for (int i = 0; i < F; ++i) z[i] -= zmax;               // sparsemax.py:32
+            if (trs) TBN_TRACE(3001 + 8 * s);
+            // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1) / |{z > tau}|,
+            // monotone from any lower bound of tau*; its support equals the
+            // reference's sort/cumsum/count k (sparsemax.py:33-39).  Start from
+            // max(-1, (sum z - 1)/F) (the max alone; all elements), nudged down
+            // by 2^-20 relative so rounding cannot push it above tau*.
+            const float bound = (zsum - (float)F * zmax - 1.0f) * (1.0f / (float)F);
+            tau = fmaxf(-1.0f, bound - 9.5367431640625e-07f * fmaxf(1.0f, fabsf(bound)));
+            float cnt_prev = (float)(F + 1);
+            for (int it = 0; it <= F; ++it) {
+              float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
+#pragma unroll
+              for (int i = 0; i + 1 < F; i += 2) {
+                const float2 m = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
+                if ((i / 2) % 2 == 0) {
+                  sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
+                  ca = __fadd2_rn(ca, m);
+                } else {
+                  sb = __ffma2_rn(m, f2(z[i], z[i + 1]), sb);
+                  cb = __fadd2_rn(cb, m);
+                }
               }
-            }
-            const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
-            float sm = s2.x + s2.y, c = c2.x + c2.y;
-            if constexpr (NF % 2) {
-              const float m = z[NF - 1] > tau ? 1.0f : 0.0f;
-              sm = fmaf(m, z[NF - 1], sm);
-              c += m;
-            }
-            const float2 o = xchg(sm, c);
-            sm += o.x;
-            c += o.y;
-            if (!done) {
-              if (c >= cnt_prev) {
-                done = true;
-              } else {
-                cnt_prev = c;
-                tau = __fdividef(sm - 1.0f, c);                       // sparsemax.py:39
+              const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
+              float sm = s2.x + s2.y, c = c2.x + c2.y;
+              if constexpr (F % 2) {
+                const float m = z[F - 1] > tau ? 1.0f : 0.0f;
+                sm = fmaf(m, z[F - 1], sm);
+                c += m;
               }
+              if (c >= cnt_prev) break;
+              cnt_prev = c;
+              tau = __fdividef(sm - 1.0f, c);                         // sparsemax.py:39
             }
-            if (__all_sync(0xffffffffu, done)) break;
+            xchg(zmax, tau);                                         // -> half 1
+          } else {
+            const float2 o = xchg(0.0f, 0.0f);
+            zmax = o.x;
+            tau = o.y;
+#pragma unroll
+            for (int i = 0; i < NZ; ++i) z[i] -= zmax;
           }
           if (trs) TBN_TRACE(3002 + 8 * s);
+          ptx::tmem_ld_wait();                                       // xnv
           claim_ts();
           if (trs) TBN_TRACE(3003 + 8 * s);
           // own features: mask, prior update, xm -> A (network.py:237-238, :246);
-          // A columns [HB, HB + KH) incl. zero padding up to K1
+          // A elements [HB, HB + KH) incl. the ones column and zero padding up to K1
           chunked<KH>([&](auto o, auto l) {
             constexpr int O = decltype(o)::value, L = decltype(l)::value;
             constexpr int FB = HB + O;
             constexpr int LF = (FB + L <= F) ? L : (FB < F ? F - FB : 0);
+            constexpr int ZO = FB - ZB;                               // index into z / pr
             float prn[L], xm[L];
 #pragma unroll
             for (int i = 0; i < L; ++i) {
               const int f = FB + i;
               if (f < F) {
-                const float m = fmaxf(z[O + i] - tau, 0.0f);          // sparsemax.py:40
-                prn[i] = pr[O + i] * (p.gamma - m);                   // network.py:237
+                const float m = fmaxf(z[ZO + i] - tau, 0.0f);         // sparsemax.py:40
+                prn[i] = pr[ZO + i] * (p.gamma - m);                  // network.py:237
                 xm[i] = m * xnv[O + i];                               // network.py:238
                 ts_at(f) = m;
               } else {
@@ -862,32 +896,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         transform(s, [&] {
           if (a.masks) flush_rows(a.masks + ((int64_t)(s - 1) * a.rows + r0) * F, nrows);
         });
-        // d = relu(f[:, :n_d]); d_sum += d; eta = sum(d); agg += eta*m (network.py:241-245)
-        if (half == 0) {
-          float eta = 0.0f;
-#pragma unroll
-          for (int i = 0; i < HH; ++i) {
-            const float d = fmaxf(prev[i], 0.0f);
-            dsum[i] += d;
-            eta += d;
-          }
-          // While every eta so far is 0, agg holds sum_s m instead (needed only for
-          // the importance fallback, network.py:259-261, which fires exactly then);
-          // the first eta > 0 resets it to eta*m, identical to the reference's sum.
-          const bool reset = all_eta_zero && eta > 0.0f;
-          const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
-          all_eta_zero = all_eta_zero && !(eta > 0.0f);
-          chunked<F>([&](auto o, auto l) {
-            constexpr int O = decltype(o)::value, L = decltype(l)::value;
-            float ag[L];
-            tmem_load_n<L>(tAG + O, ag);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < L; ++i) ag[i] = fmaf(w, ts_at(O + i), reset ? 0.0f : ag[i]);
-            tmem_store_n<L>(tAG + O, ag);
-          });
-        }
+        agg_pending = true;
       }
+      agg_update();                        // the last step's (no att GEMM follows)
       // ---- head + softmax + argmax (network.py:253-256, :279), importance
       // = agg / sum(agg) or mean_s(masks) (network.py:258-261): half 0 ----
       float ag[F];

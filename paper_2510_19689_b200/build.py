@@ -29,6 +29,8 @@ CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-v", "--expt-relaxed-constexpr",
                             "-Xcompiler", "-Wall"]
 if os.environ.get("TBN_TRACE_BUILD"):          # development timeline build (see tools/trace_run.py)
     CU_FLAGS += ["-DTBN_ENABLE_TRACE"]
+if os.environ.get("TBN_EXTRA_FLAGS"):          # development A/B variants (tools/ab.sh)
+    CU_FLAGS += os.environ["TBN_EXTRA_FLAGS"].split()
 CXX = shutil.which("g++") or "g++"
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 

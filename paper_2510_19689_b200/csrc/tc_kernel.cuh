@@ -540,6 +540,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       if (!is_att) seg_acquire(false);
       // one warp polls the accumulator barrier; the rest sleep in bar.sync
       if ((warp & 7) == 0) ptx::mbar_wait(&bars->dfull[g], dphase);
+      if (tr && issuer) TBN_TRACE(gofs + 3500 + j);
       dphase ^= 1;
       ptx::named_bar_sync(bar_id, 256);
       ptx::tc_fence_after();
@@ -619,21 +620,26 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       }
       ptx::named_bar_sync(bar_id, 256);
     };
-    // (a, b) exchange with the partner warp of the same lane quarter (the other
-    // column half): double-buffered by parity, one 64-thread barrier each.
+    // half 0 -> half 1 hand-off with the partner warp of the same lane quarter
+    // (the other column half): double-buffered by parity, one 64-thread
+    // barrier each.  Slot (par, 0) carries (max z, tau); slot (par, 1).x carries
+    // the step's eta, written before the attentive GEMM's barrier.
     float4* xb4 = reinterpret_cast<float4*>(smem + SM::OFF_XCH) + g * 512;
     const uint32_t pair_bar = 3 + g * 4 + (warp & 3);
     uint32_t xpar = 0;
-    auto xchg4 = [&](float va, float vb, float vc) -> float4 {
-      xb4[(xpar * 2 + half) * 128 + t] = make_float4(va, vb, vc, 0.0f);
+    auto send_tau = [&](float zmax, float tau) {
+      xb4[(xpar * 2) * 128 + t] = make_float4(zmax, tau, 0.0f, 0.0f);
       ptx::named_bar_sync(pair_bar, 64);
-      const float4 o = xb4[(xpar * 2 + (half ^ 1)) * 128 + t];
       xpar ^= 1;
-      return o;
     };
-    auto xchg = [&](float va, float vb) -> float2 {
-      const float4 o = xchg4(va, vb, 0.0f);
+    auto recv_tau = [&]() -> float2 {
+      ptx::named_bar_sync(pair_bar, 64);
+      const float4 o = xb4[(xpar * 2) * 128 + t];
+      xpar ^= 1;
       return f2(o.x, o.y);
+    };
+    auto eta_slot = [&]() -> float& {
+      return reinterpret_cast<float*>(xb4 + (xpar * 2 + 1) * 128 + t)[0];
     };
     auto ts_at = [&](int f) -> float& {
       if constexpr (CF::DENSE_IO) return ts[t * F + f];
@@ -651,9 +657,16 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
 
       // ---- x tile (TMA-staged): xn = (x - mean) * rsqrt(var + eps) for this
       // half's features (network.py:118-120); prior = 1; agg = 0 ----
+      const bool trt = (g == 0 && pair == blockIdx.x && issuer);
+      if (trt) TBN_TRACE(3090);
       ptx::mbar_wait(&bars->xfull[g], xphase);
       xphase ^= 1;
+      if (trt) TBN_TRACE(3091);
+#ifdef TBN_NO_TOKEN       // ablation: free-running groups (measured slower)
+      paired = false;
+#else
       paired = (NG == 2) && (pair * NG + 1 < ntiles);
+#endif
       seg_acquire(true);
       {
         const int ne = nrows * F;
@@ -670,6 +683,15 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           }
           ptx::named_bar_sync(bar_id, 256);
         }
+        if constexpr (CF::DENSE_IO) {
+          if (!full_tile) {     // the last, partial tile: complete the staging tile in SMEM
+            float* xw = const_cast<float*>(xs);
+            for (int e = nbulk + (int)(threadIdx.x % 256); e < 128 * F; e += 256)
+              xw[e] = e < ne ? __ldg(a.x + r0 * F + e) : 0.0f;
+            ptx::fence_async_shared();          // generic writes before the next TMA refill
+            ptx::named_bar_sync(bar_id, 256);
+          }
+        }
         int bad = 0;
         auto xn_half = [&](auto hc) {
           constexpr int HB = decltype(hc)::value;
@@ -684,15 +706,13 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
               one[i] = 1.0f;
               if (f < F) {
                 float xv;
-                if constexpr (CF::DENSE_IO) {
-                  const int e = t * F + f;
-                  if (full_tile) xv = xs[e];
-                  else xv = (e < nbulk) ? xs[e] : (e < ne ? __ldg(a.x + r0 * F + e) : 0.0f);
-                } else {
-                  xv = ts[f * 129 + t];
-                }
+                if constexpr (CF::DENSE_IO) xv = xs[t * F + f];
+                else xv = ts[f * 129 + t];
                 bad |= !isfinite(xv);
-                xn[i] = a.normalized ? xv : (xv - shift[f]) * scale[f];
+                // normalized input: (x - 0) * 1 == x exactly; no branch per element
+                const float sh = a.normalized ? 0.0f : shift[f];
+                const float sc = a.normalized ? 1.0f : scale[f];
+                xn[i] = (xv - sh) * sc;
               } else {
                 xn[i] = (f == F) ? 1.0f : 0.0f;                       // ones column (bias row)
               }
@@ -718,10 +738,13 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         }
         if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
       }
+      if (trt) TBN_TRACE(3092);
       float prev[HH];
-      float dsum[HH];                            // half 0: d_sum (n_d == H/2)
+      // half 0: the head is linear, so logits = sum_s relu(d_s) @ head_W + b
+      // (network.py:244, :253) accumulates per step: C registers instead of n_d
+      float lacc[C];
 #pragma unroll
-      for (int i = 0; i < HH; ++i) dsum[i] = 0.0f;
+      for (int c = 0; c < C; ++c) lacc[c] = 0.0f;
       bool all_eta_zero = true;
 
       // feature transformer (network.py:124-141): 4 GEMM+GLU blocks
@@ -744,20 +767,23 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       // (network.py:241-245) for the step just finished (half 0 owns d, agg).
       // Runs in the next attentive GEMM's shadow (its post hook).
       bool agg_pending = false;
-      auto agg_update = [&]() {
-        if (!agg_pending) return;
-        agg_pending = false;
-        if (half != 0) return;
+      // eta = sum(d) and d_sum (half 0, which holds d); the agg weights with the
+      // importance-fallback bookkeeping: while every eta so far is 0, agg holds
+      // sum_s m instead (needed only for the fallback, network.py:259-261, which
+      // fires exactly then); the first eta > 0 resets it to eta*m, identical to
+      // the reference's sum.  Both halves track all_eta_zero from the same eta.
+      auto step_eta = [&]() -> float {
         float eta = 0.0f;
 #pragma unroll
         for (int i = 0; i < HH; ++i) {
           const float d = fmaxf(prev[i], 0.0f);
-          dsum[i] += d;
+#pragma unroll
+          for (int c = 0; c < C; ++c) lacc[c] = fmaf(d, cst[CF::C_HW + i * C + c], lacc[c]);
           eta += d;
         }
-        // While every eta so far is 0, agg holds sum_s m instead (needed only for
-        // the importance fallback, network.py:259-261, which fires exactly then);
-        // the first eta > 0 resets it to eta*m, identical to the reference's sum.
+        return eta;
+      };
+      auto agg_apply = [&](float eta) {
         const bool reset = all_eta_zero && eta > 0.0f;
         const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
         all_eta_zero = all_eta_zero && !(eta > 0.0f);
@@ -771,6 +797,21 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           tmem_store_n<L>(tAG + O, ag);
         });
       };
+      // Under the attentive GEMM (its post hook): half 0 finishes the previous
+      // step's d (network.py:241-244) and hands eta to half 1, which applies
+      // agg += eta*m (network.py:245) while half 0 runs the tau search.
+      auto agg_post = [&]() {
+        if (half != 0 || !agg_pending) return;
+        agg_pending = false;
+        const float eta = step_eta();
+        eta_slot() = eta;
+        all_eta_zero = all_eta_zero && !(eta > 0.0f);
+      };
+      auto agg_half1 = [&]() {
+        if (!agg_pending) return;
+        agg_pending = false;
+        agg_apply(eta_slot());
+      };
 
       transform(0, nopost);                                           // network.py:226-227
       for (int s = 1; s <= S; ++s) {
@@ -781,7 +822,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
           for (int k = 0; k < CF::KATT; ++k) av[k] = k < NA ? prev[k] : (k == NA ? 1.0f : 0.0f);
           store_a_all<CF, CF::KATT>(tA, tAL, av);
         }
-        gemm(j++, pair, agg_update);        // previous step's eta/agg under the att MMA
+        gemm(j++, pair, agg_post);          // previous step's d/eta under the att MMA
         const bool trs = (g == 0 && pair == blockIdx.x && issuer);
         if (trs) TBN_TRACE(3000 + 8 * s);
         // attentive FC + prior + sparsemax (network.py:233-236, sparsemax.py:13-41),
@@ -851,9 +892,10 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
               cnt_prev = c;
               tau = __fdividef(sm - 1.0f, c);                         // sparsemax.py:39
             }
-            xchg(zmax, tau);                                         // -> half 1
+            send_tau(zmax, tau);                                     // -> half 1
           } else {
-            const float2 o = xchg(0.0f, 0.0f);
+            agg_half1();                                             // in the tau search's shadow
+            const float2 o = recv_tau();
             zmax = o.x;
             tau = o.y;
 #pragma unroll
@@ -898,7 +940,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         });
         agg_pending = true;
       }
-      agg_update();                        // the last step's (no att GEMM follows)
+      if (agg_pending && half == 0) agg_apply(step_eta());   // the last step's (no att GEMM follows)
+      agg_pending = false;
+      if (trt) TBN_TRACE(3100);
       // ---- head + softmax + argmax (network.py:253-256, :279), importance
       // = agg / sum(agg) or mean_s(masks) (network.py:258-261): half 0 ----
       float ag[F];
@@ -908,10 +952,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         float lmax = -INFINITY;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          float acc = 0.0f;
-#pragma unroll
-          for (int k = 0; k < ND; ++k) acc = fmaf(dsum[k], cst[CF::C_HW + k * C + c], acc);
-          lg[c] = acc + cst[CF::C_HB + c];
+          lg[c] = lacc[c] + cst[CF::C_HB + c];
           lmax = fmaxf(lmax, lg[c]);
         }
         float ex[C], es = 0.0f;
@@ -937,7 +978,9 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         div = all_eta_zero ? (float)S : tot;
         rdiv = __frcp_rn(div);
       }
+      if (trt) TBN_TRACE(3101);
       claim_ts();
+      if (trt) TBN_TRACE(3102);
       if (half == 0) {
 #pragma unroll
         for (int f = 0; f < F; ++f) ts_at(f) = ag[f] * rdiv;
@@ -945,6 +988,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
       if constexpr (CF::DENSE_IO) ptx::fence_async_shared();
       ptx::named_bar_sync(bar_id, 256);
       if (a.importance) flush_rows(a.importance + r0 * F, nrows);
+      if (trt) TBN_TRACE(3103);
       seg_release();
       if (paired && g == 0) ptx::named_bar_sync(11, 512);   // consume group 1's last handoff
     }

@@ -1,0 +1,517 @@
+// k2_kernel.cuh — K2: the whole TabNet forward (network.py:195-267) as ONE
+// persistent sm_100a kernel, thread-per-row, for the single-pass tensor-core
+// modes (TF32, BF16).
+//
+// Why a second design next to K1 (tc_kernel.cuh): K1 keeps each row's whole
+// state (xn, prior, agg) in TMEM and splits a row over two threads, which
+// leaves room for only 2 row tiles per SM; its per-tile chain of 29 GEMM ->
+// epilogue hand-offs is then latency-bound (~70k cycles per tile pair, ~40%
+// issue).  K2 moves the per-row state into registers (one thread owns one
+// row: xn, agg, the GLU activations) and keeps only the MMA operands and the
+// prior in TMEM, so 3-4 independent row groups (128 rows each) share an SM
+// and hide each other's MMA/TMEM latency without any inter-group token.
+//
+//   TMEM (per row group, 128 lanes)        SMEM (per CTA)
+//   [D accumulator  DW cols]               consts: affine, head
+//   [A operand      KA cols]               ALL weight blocks, resident (one
+//   [prior          F  cols]                 bulk load per CTA)
+//                                          per warp: a 32 x F row tile staging
+//   registers (per row): xn[F], agg[F],      x on the way in, each step's mask
+//   the GLU activations g[H], logits[C]      and the importance on the way out
+//
+// GLU uses sigma(u) = (1 + tanh(u/2)) / 2 (one MUFU op per element): the
+// packer folds the 1/2 (and the residual sqrt(1/2), network.py:131-137) into
+// the weights and biases, so one GLU element is tanh + 2 FFMA:
+//   out = lin'(1 + t) + sqrt(.5) prev,   lin' = (sqrt(.5)) u_lin / 2,  t = tanh(u_gate / 2)
+// Biases ride in the GEMMs (a ones column in A, a bias row in B).
+//
+// Per-row arithmetic is identical for every row whatever the batch size, tile
+// position, grid or group: the batch-invariance contract (network.py:11-14).
+#pragma once
+#include <cstdint>
+#include <type_traits>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include "tc_kernel.cuh"
+
+namespace tbn {
+namespace k2 {
+
+using tc::chunked;
+using tc::cmax;
+using tc::kPrecBF16;
+using tc::kPrecTF32;
+using tc::kR;
+using tc::rup;
+using tc::tmem_load_n;
+using tc::tmem_store_n;
+
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
+constexpr int pow2ceil(int v) { int p = 32; while (p < v) p <<= 1; return p; }
+
+template <int F_, int ND_, int NA_, int S_, int C_, int PREC_>
+struct Cfg {
+  static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
+  static_assert(PREC == kPrecTF32 || PREC == kPrecBF16, "K2 covers the single-pass modes");
+  static constexpr int H = ND + NA, N2 = 2 * H;
+  static constexpr bool X3 = false;
+  static constexpr bool BF = (PREC == kPrecBF16);
+  static constexpr int KG = BF ? 16 : 8;               // MMA K granule
+  static constexpr int ESZ = BF ? 2 : 4;
+  // bias as an extra K row of B times a ones column of A at index F / H / NA
+  static constexpr int K1 = rup(F + 1, KG);
+  static constexpr int KHID = rup(H + 1, KG);
+  static constexpr int KATT = rup(NA + 1, KG);
+  static constexpr int FN = rup(F, 16);                // attentive N
+  static constexpr int KA_EL = cmax(cmax(K1, KHID), KATT);
+  static constexpr int KA = BF ? KA_EL / 2 : KA_EL;    // A operand TMEM columns
+  static constexpr int DW = cmax(N2, FN);
+  static constexpr int T_D = 0, T_A = DW, T_PR = DW + KA, T_END = T_PR + F;
+  static constexpr int TCG = rup(T_END, 32);           // TMEM columns per group
+  // groups per CTA: TMEM and the register file (a row's live state is about
+  // 2F + H + 48 registers) both have to fit
+  static constexpr int REGS_ROW = 2 * F + H + 48;
+  static constexpr int NG_TMEM = 512 / TCG;
+  static constexpr int NG_REG = 65536 / (128 * REGS_ROW);
+  static constexpr int NG = cmin(4, cmin(NG_TMEM, NG_REG));
+  static_assert(NG >= 1, "per-row state does not fit");
+  static constexpr int TCOLS = pow2ceil(NG * TCG);
+  static_assert(TCOLS <= 512, "TMEM");
+  static_assert(N2 <= 256 && FN <= 256, "MMA N > 256");
+  static constexpr int THREADS = NG * 128;
+  static constexpr int NW = NG * 4;
+  // weight blocks (B operands, N x K K-major canonical)
+  static constexpr int B_SH1 = N2 * K1 * ESZ;
+  static constexpr int B_HID = N2 * KHID * ESZ;
+  static constexpr int B_ATT = FN * KATT * ESZ;
+  // consts (floats): scale F | shift F | head_W ND*C | head_b C
+  static constexpr int C_SCALE = 0, C_SHIFT = rup(F, 4), C_HW = C_SHIFT + rup(F, 4);
+  static constexpr int C_HB = C_HW + rup(ND * C, 4), C_END = rup(C_HB + C, 4);
+  static constexpr int CONST_BYTES = C_END * 4;
+  // image: [consts][sh1][sh2][fc1_0..S][fc2_0..S][att_1..S], 128-B aligned blocks
+  static constexpr int O_SH1 = rup(CONST_BYTES, 128);
+  static constexpr int O_SH2 = O_SH1 + rup(B_SH1, 128);
+  static constexpr int O_FC1 = O_SH2 + rup(B_HID, 128);
+  static constexpr int O_FC2 = O_FC1 + (S + 1) * rup(B_HID, 128);
+  static constexpr int O_ATT = O_FC2 + (S + 1) * rup(B_HID, 128);
+  static constexpr int IMG_BYTES = O_ATT + S * rup(B_ATT, 128);
+  static constexpr int STG = rup(32 * F * 4, 128);     // per-warp row staging
+  static constexpr int OFF_STG = rup(IMG_BYTES, 1024);
+  static constexpr int OFF_BAR = OFF_STG + NW * STG;
+  static constexpr int SMEM_BYTES = OFF_BAR + 256;
+  static_assert(SMEM_BYTES <= 227 * 1024, "weights + staging exceed shared memory");
+};
+
+struct Params {
+  const uint8_t* wimg;     // device image (layout above)
+  float gamma;
+};
+
+struct Bars {
+  uint64_t cfull;
+  uint64_t dfull[4];       // per group: MMA chain complete
+  uint64_t xfull[16];      // per warp: x row tile landed
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// A operand: L elements of v starting at element E (E, L even for bf16)
+template <class CF, int E, int L, int M>
+__device__ __forceinline__ void put_a(uint32_t tA, const float (&v)[M]) {
+  if constexpr (CF::BF) {
+    static_assert(E % 2 == 0 && L % 2 == 0, "bf16 A elements come in pairs");
+    float pk[L / 2];
+#pragma unroll
+    for (int i = 0; i < L / 2; ++i) {
+      const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);   // low = even
+      pk[i] = *reinterpret_cast<const float*>(&b);
+    }
+    tmem_store_n<L / 2>(tA + E / 2, pk);
+  } else {
+    tmem_store_n<L>(tA + E, v);
+  }
+}
+// A elements [E, E+L) = ones at element E, zeros after (the bias column)
+template <class CF, int E, int L>
+__device__ __forceinline__ void put_ones(uint32_t tA) {
+  float v[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) v[i] = i == 0 ? 1.0f : 0.0f;
+  put_a<CF, E, L>(tA, v);
+}
+
+template <class CF>
+__global__ void __launch_bounds__(CF::THREADS, 1)
+tabnet_rowthread(const Params p, const ForwardArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int F = CF::F, H = CF::H, ND = CF::ND, NA = CF::NA, S = CF::S, C = CF::C, NG = CF::NG;
+  const float* cst = reinterpret_cast<const float*>(smem);
+  Bars* bars = reinterpret_cast<Bars*>(smem + CF::OFF_BAR);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp >> 2, q = warp & 3;
+  const int t = q * 32 + lane;                      // row within the tile == TMEM lane
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const bool x_bulk_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0);
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bars->cfull, 1);
+    for (int i = 0; i < NG; ++i) ptx::mbar_init(&bars->dfull[i], 1);
+    for (int i = 0; i < CF::NW; ++i) ptx::mbar_init(&bars->xfull[i], 1);
+    ptx::fence_mbar_init();
+    ptx::mbar_arrive_expect_tx(&bars->cfull, CF::IMG_BYTES);
+    constexpr int CH = 32768;
+    for (int o = 0; o < CF::IMG_BYTES; o += CH)
+      ptx::bulk_g2s(smem + o, p.wimg + o, (uint32_t)(CF::IMG_BYTES - o < CH ? CF::IMG_BYTES - o : CH),
+                    &bars->cfull);
+  }
+  if (warp == 0) ptx::tmem_alloc<CF::TCOLS>(&bars->tmem_base);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tg = bars->tmem_base + (uint32_t)(g * CF::TCG) + ((uint32_t)(q * 32) << 16);
+  const uint32_t tD = tg + CF::T_D, tA = tg + CF::T_A, tPR = tg + CF::T_PR;
+  float* stg = reinterpret_cast<float*>(smem + CF::OFF_STG + warp * CF::STG);
+  const uint32_t bar_id = 1 + g;
+  uint32_t dphase = 0, xphase = 0;
+
+  // stage this warp's rows [r0w, r0w + nw) of x into stg (TMA bulk + tail)
+  auto load_x = [&](int64_t r0w, int nw) {
+    const int ne = nw * F;
+    const int nb = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
+    if (lane == 0) {
+      if (nb > 0) {
+        ptx::mbar_arrive_expect_tx(&bars->xfull[warp], (uint32_t)nb * 4u);
+        ptx::bulk_g2s(stg, a.x + r0w * F, (uint32_t)nb * 4u, &bars->xfull[warp]);
+      } else {
+        ptx::mbar_arrive(&bars->xfull[warp]);
+      }
+    }
+    for (int e = nb + lane; e < 32 * F; e += 32) stg[e] = e < ne ? __ldg(a.x + r0w * F + e) : 0.0f;
+    ptx::mbar_wait(&bars->xfull[warp], xphase);
+    xphase ^= 1;
+    __syncwarp();
+  };
+  // stg (32 x F, this warp's rows) -> dst rows [0, nw): bulk store when aligned
+  auto flush = [&](float* dst, int nw) {
+    const int ne = nw * F;
+    const bool al = ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+    const int nb = al ? ((ne * 4) & ~15) / 4 : 0;
+    ptx::fence_async_shared();
+    __syncwarp();
+    if (lane == 0 && nb > 0) {
+      ptx::bulk_s2g(dst, stg, (uint32_t)nb * 4u);
+      ptx::bulk_commit();
+    }
+    for (int e = nb + lane; e < ne; e += 32) dst[e] = stg[e];
+  };
+  auto claim_stg = [&]() {      // the previous bulk store has finished reading stg
+    if (lane == 0) ptx::bulk_wait_read0();
+    __syncwarp();
+  };
+
+  ptx::mbar_wait(&bars->cfull, 0);
+  if (a.scale) {     // batch-statistics control: override the affine in this CTA's copy
+    float* cw = reinterpret_cast<float*>(smem);
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+      cw[CF::C_SCALE + f] = a.scale[f];
+      cw[CF::C_SHIFT + f] = a.shift[f];
+    }
+  }
+  __syncthreads();
+
+  const uint32_t wbase = ptx::smem_u32(smem);
+  // One GEMM: A (this group's TMEM) x B (resident block at byte offset bo).
+  // The group meets at its barrier, warp 0 of the group issues the chain and
+  // commits it; `post` overlaps the MMA; then everyone waits for D.
+  int jt = 0;                                    // trace: GEMM counter
+  const bool tr = (q == 0 && lane == 0);
+  auto gemm = [&](int kind, uint32_t bo, auto&& post) {
+    if (tr) TBN_TRACE(g * 4000 + 4 * jt);
+    ptx::tmem_st_wait();
+    ptx::tc_fence_before();
+    ptx::named_bar_sync(bar_id, 128);
+    if (tr) TBN_TRACE(g * 4000 + 4 * jt + 1);
+    if (q == 0) {
+      ptx::tc_fence_after();
+      if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tA, wbase + bo);
+      else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tA, wbase + bo);
+      else tc::issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tA, wbase + bo);
+      ptx::mma_commit(&bars->dfull[g]);
+    }
+    if (tr) TBN_TRACE(g * 4000 + 4 * jt + 2);
+    post();
+    ptx::mbar_wait(&bars->dfull[g], dphase);
+    dphase ^= 1;
+    ptx::tc_fence_after();
+    if (tr) TBN_TRACE(g * 4000 + 4 * jt + 3);
+    ++jt;
+  };
+  auto nopost = [] {};
+
+  float xn[F], agg[F], gv[H], lacc[C];
+
+  // GLU block over D = [lin' | gate'] (H + H columns): gv <- lin'(1+t) [+ R gv]
+  auto glu = [&](bool residual) {
+    constexpr int CW = H < 16 ? H : 16;
+    static_assert(H % CW == 0, "GLU chunking");
+    float lin[CW], gate[CW];
+    tmem_load_n<CW>(tD, lin);
+    tmem_load_n<CW>(tD + H, gate);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int c0 = 0; c0 < H; c0 += CW) {
+      float ln2[CW], gt2[CW];
+      if (c0 + CW < H) {           // next chunk in flight while this one computes
+        tmem_load_n<CW>(tD + c0 + CW, ln2);
+        tmem_load_n<CW>(tD + H + c0 + CW, gt2);
+      }
+#pragma unroll
+      for (int i = 0; i < CW; i += 2) {
+        const float2 th = f2(tanh_approx(gate[i]), tanh_approx(gate[i + 1]));
+        const float2 l = f2(lin[i], lin[i + 1]);
+        float2 w = l;
+        if (residual) w = __ffma2_rn(f2(gv[c0 + i], gv[c0 + i + 1]), f2(kR, kR), l);
+        const float2 o = __ffma2_rn(l, th, w);
+        gv[c0 + i] = o.x;
+        gv[c0 + i + 1] = o.y;
+      }
+      if (c0 + CW < H) {
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < CW; ++i) { lin[i] = ln2[i]; gate[i] = gt2[i]; }
+      }
+    }
+  };
+  auto store_g = [&]() { put_a<CF, 0, H>(tA, gv); };
+
+  for (int64_t k = 0;; ++k) {
+    const int64_t tile = (int64_t)blockIdx.x + (int64_t)gridDim.x * (g + (int64_t)NG * k);
+    if (tile >= ntiles) break;
+    const int64_t r0 = tile * 128;
+    const int nrows = (int)(a.rows - r0 < 128 ? a.rows - r0 : 128);
+    const int nw = nrows - q * 32 < 0 ? 0 : (nrows - q * 32 > 32 ? 32 : nrows - q * 32);
+    const bool valid = lane < nw;
+    const int64_t row = r0 + t;
+    const int64_t r0w = r0 + q * 32;
+
+    // ---- x -> xn (network.py:118-120), prior = 1, agg = 0 ----
+    if (tr) TBN_TRACE(g * 4000 + 3000 + 8 * (int)k);
+    claim_stg();
+    ptx::fence_async_shared();
+    __syncwarp();
+    if (nw > 0) load_x(r0w, nw);
+    if (tr) TBN_TRACE(g * 4000 + 3001 + 8 * (int)k);
+    {
+      int bad = 0;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const float xv = nw > 0 ? stg[lane * F + f] : 0.0f;
+        bad |= !isfinite(xv);
+        const float sh = a.normalized ? 0.0f : cst[CF::C_SHIFT + f];
+        const float sc = a.normalized ? 1.0f : cst[CF::C_SCALE + f];
+        xn[f] = (xv - sh) * sc;
+        agg[f] = 0.0f;
+      }
+      if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
+      float one[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) one[f] = 1.0f;
+      tmem_store_n<F>(tPR, one);
+      float av[CF::K1];
+#pragma unroll
+      for (int e = 0; e < CF::K1; ++e) av[e] = e < F ? xn[e] : (e == F ? 1.0f : 0.0f);
+      put_a<CF, 0, CF::K1>(tA, av);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) lacc[c] = 0.0f;
+    bool all_eta_zero = true;
+
+    // feature transformer (network.py:124-141)
+    auto transform = [&](int s, auto&& post_first) {
+      const uint32_t o1 = CF::O_FC1 + (uint32_t)s * rup(CF::B_HID, 128);
+      const uint32_t o2 = CF::O_FC2 + (uint32_t)s * rup(CF::B_HID, 128);
+      gemm(0, CF::O_SH1, post_first);
+      glu(false);
+      store_g();
+      put_ones<CF, H, CF::KHID - H>(tA);        // hidden-GEMM bias column
+      gemm(1, CF::O_SH2, nopost);
+      glu(true);
+      store_g();
+      gemm(1, o1, nopost);
+      glu(true);
+      store_g();
+      gemm(1, o2, nopost);
+      glu(true);
+    };
+    // d = relu(f[:, :n_d]); eta = sum d; logits accumulate (the head is linear,
+    // network.py:244, :253)
+    auto step_eta = [&]() -> float {
+      float e0 = 0.0f, e1 = 0.0f;
+#pragma unroll
+      for (int i = 0; i < ND; ++i) {
+        const float d = fmaxf(gv[i], 0.0f);
+#pragma unroll
+        for (int c = 0; c < C; ++c) lacc[c] = fmaf(d, cst[CF::C_HW + i * C + c], lacc[c]);
+        if (i & 1) e1 += d; else e0 += d;
+      }
+      return e0 + e1;
+    };
+    // agg += eta * m (network.py:245) from the staged mask; while every eta so
+    // far is 0 agg holds sum_s m instead, which is exactly the importance
+    // fallback's numerator (network.py:259-261); the first eta > 0 resets it.
+    auto agg_apply = [&](float eta) {
+      const bool reset = all_eta_zero && eta > 0.0f;
+      const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
+      all_eta_zero = all_eta_zero && !(eta > 0.0f);
+#pragma unroll
+      for (int f = 0; f < F; ++f) agg[f] = fmaf(w, stg[lane * F + f], reset ? 0.0f : agg[f]);
+    };
+
+    transform(0, nopost);                                        // network.py:226-227
+    float eta_prev = 0.0f;
+    for (int s = 1; s <= S; ++s) {
+      // A <- [a = f[:, n_d:], 1, 0..]; under the attentive MMA: the previous
+      // step's d/eta/logits and agg update
+      {
+        float av[CF::KATT];
+#pragma unroll
+        for (int e = 0; e < CF::KATT; ++e) av[e] = e < NA ? gv[ND + e] : (e == NA ? 1.0f : 0.0f);
+        if (s > 1) eta_prev = step_eta();
+        put_a<CF, 0, CF::KATT>(tA, av);
+      }
+      gemm(2, CF::O_ATT + (uint32_t)(s - 1) * rup(CF::B_ATT, 128), [&] {
+        if (s > 1) agg_apply(eta_prev);
+      });
+      // attentive transformer + sparsemax (network.py:233-238, sparsemax.py:13-41)
+      float z[F];
+      {
+        float pr[F];
+        tmem_load_n<F>(tD, z);
+        tmem_load_n<F>(tPR, pr);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < F; ++i) z[i] = pr[i] * z[i];           // bias already in D
+      }
+      float zmax, tau;
+      if (tr) TBN_TRACE(g * 4000 + 3500 + 4 * s);
+      {
+        float m0 = -INFINITY, m1 = -INFINITY, s0 = 0.0f, s1 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+          if (i & 1) { m1 = fmaxf(m1, z[i]); s1 += z[i]; }
+          else { m0 = fmaxf(m0, z[i]); s0 += z[i]; }
+        }
+        zmax = fmaxf(m0, m1);
+        const float zsum = s0 + s1;
+#pragma unroll
+        for (int i = 0; i < F; ++i) z[i] -= zmax;                  // sparsemax.py:32
+        // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1)/|{z > tau}|, monotone
+        // from a lower bound; its support equals the reference's sort/cumsum/count
+        // k (sparsemax.py:33-39).  Start: max(-1, (sum z - 1)/F) nudged down 2^-20.
+        const float bound = (zsum - (float)F * zmax - 1.0f) * (1.0f / (float)F);
+        tau = fmaxf(-1.0f, bound - 9.5367431640625e-07f * fmaxf(1.0f, fabsf(bound)));
+        float cnt_prev = (float)(F + 1);
+        for (int it = 0; it <= F; ++it) {
+          float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
+#pragma unroll
+          for (int i = 0; i + 1 < F; i += 2) {
+            const float2 m = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
+            if ((i / 2) % 2 == 0) {
+              sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
+              ca = __fadd2_rn(ca, m);
+            } else {
+              sb = __ffma2_rn(m, f2(z[i], z[i + 1]), sb);
+              cb = __fadd2_rn(cb, m);
+            }
+          }
+          const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
+          float sm = s2.x + s2.y, cn = c2.x + c2.y;
+          if constexpr (F % 2) {
+            const float m = z[F - 1] > tau ? 1.0f : 0.0f;
+            sm = fmaf(m, z[F - 1], sm);
+            cn += m;
+          }
+          if (cn >= cnt_prev) break;
+          cnt_prev = cn;
+          tau = __fdividef(sm - 1.0f, cn);                            // sparsemax.py:39
+        }
+      }
+      // mask, prior update, x*mask -> A; mask -> staging (network.py:236-238, :246)
+      if (tr) TBN_TRACE(g * 4000 + 3501 + 4 * s);
+      claim_stg();
+      {
+        float pr[F];
+        tmem_load_n<F>(tPR, pr);
+        ptx::tmem_ld_wait();
+        float av[CF::K1];
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          const float m = fmaxf(z[f] - tau, 0.0f);                   // sparsemax.py:40
+          pr[f] = pr[f] * (p.gamma - m);                             // network.py:237
+          av[f] = m * xn[f];                                         // network.py:238
+          stg[lane * F + f] = m;
+        }
+#pragma unroll
+        for (int e = F; e < CF::K1; ++e) av[e] = e == F ? 1.0f : 0.0f;
+        tmem_store_n<F>(tPR, pr);
+        put_a<CF, 0, CF::K1>(tA, av);
+      }
+      // masks[s-1] of this warp's rows leave while the shared1 MMA runs
+      transform(s, [&] {
+        if (a.masks && nw > 0) flush(a.masks + ((int64_t)(s - 1) * a.rows + r0w) * F, nw);
+      });
+    }
+    agg_apply(step_eta());                       // the last step (no attentive GEMM follows)
+    if (tr) TBN_TRACE(g * 4000 + 3002 + 8 * (int)k);
+
+    // ---- head + softmax + argmax (network.py:253-256, :279); importance =
+    // agg / sum(agg) or mean_s(masks) (network.py:258-261) ----
+    {
+      float lg[C], lmax = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        lg[c] = lacc[c] + cst[CF::C_HB + c];
+        lmax = fmaxf(lmax, lg[c]);
+      }
+      float ex[C], es = 0.0f;
+#pragma unroll
+      for (int c = 0; c < C; ++c) { ex[c] = expf(lg[c] - lmax); es += ex[c]; }
+      if (valid) {
+        int best = 0;
+        float bv = -1.0f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const float pv = ex[c] / es;
+          if (a.logits) a.logits[row * C + c] = lg[c];
+          if (a.probs) a.probs[row * C + c] = pv;
+          if (pv > bv) { bv = pv; best = c; }
+        }
+        if (a.pred) a.pred[row] = best;
+      }
+      float t0 = 0.0f, t1 = 0.0f;
+#pragma unroll
+      for (int f = 0; f < F; ++f) { if (f & 1) t1 += agg[f]; else t0 += agg[f]; }
+      const float div = all_eta_zero ? (float)S : (t0 + t1);
+      const float rdiv = __frcp_rn(div);
+      claim_stg();
+#pragma unroll
+      for (int f = 0; f < F; ++f) stg[lane * F + f] = agg[f] * rdiv;
+      if (a.importance && nw > 0) flush(a.importance + r0w * F, nw);
+    }
+    if (tr) TBN_TRACE(g * 4000 + 3003 + 8 * (int)k);
+  }
+  if (lane == 0) ptx::bulk_wait0();
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc<CF::TCOLS>(bars->tmem_base);
+}
+
+}  // namespace k2
+}  // namespace tbn

@@ -1,0 +1,129 @@
+// kernel_k2.cu — host side of K2 (k2_kernel.cuh): its weight packer and the
+// per-shape instances.  The image is the reference's float64 params dict
+// (network.py:81-96, used as x @ W) as B operands (N x K K-major canonical,
+// TF32 = rna(w) or BF16 = rne(w)) with the bias as an extra K row, and the GLU
+// constants folded in for the tanh form of the sigmoid:
+//   sigma(u) = (1 + tanh(u/2)) / 2   =>  gate columns x 1/2,
+//   linear columns x 1/2 (shared1) or x sqrt(1/2)/2 (the residual blocks
+//   shared2/fc1/fc2, network.py:131-137: (lin sigma + prev) sqrt(.5)).
+#include <cmath>
+#include <cstring>
+#include <vector>
+#include "tbn_tc.h"
+#include "k2_kernel.cuh"
+#include "pack_util.h"
+
+namespace tbn {
+
+namespace {
+
+struct K2Instance {
+  int F, ND, NA, S, C, prec;
+  bool (*pack)(const HostParams&, TcModel*, std::string*);
+  cudaError_t (*launch)(const TcModel&, const ForwardArgs&, int, cudaStream_t);
+};
+
+template <class CF>
+bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
+  constexpr int F = CF::F, H = CF::H, N2 = CF::N2, S = CF::S, ND = CF::ND, NA = CF::NA, C = CF::C;
+  std::vector<float> img(CF::IMG_BYTES / 4, 0.0f);
+  for (int f = 0; f < F; ++f) {
+    img[CF::C_SCALE + f] = (float)(1.0 / std::sqrt(hp.norm_var[f] + 1e-8));   // network.py:120
+    img[CF::C_SHIFT + f] = (float)hp.norm_mean[f];
+  }
+  for (int i = 0; i < ND * C; ++i) img[CF::C_HW + i] = (float)hp.head_W[i];
+  for (int i = 0; i < C; ++i) img[CF::C_HB + i] = (float)hp.head_b[i];
+  const double kR = 0.70710678118654752440;
+  std::vector<double> cs_first(N2), cs_res(N2);
+  for (int n = 0; n < N2; ++n) {
+    cs_first[n] = 0.5;
+    cs_res[n] = n < H ? 0.5 * kR : 0.5;
+  }
+  using pack::pack_block;
+  constexpr int HB = tc::rup(CF::B_HID, 128);
+  pack_block(img, CF::O_SH1 / 4, hp.sh1_W, F, N2, N2, CF::K1, false, N2, &cs_first, hp.sh1_b, CF::BF);
+  pack_block(img, CF::O_SH2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, false, N2, &cs_res, hp.sh2_b, CF::BF);
+  for (int s = 0; s <= S; ++s) {
+    pack_block(img, (CF::O_FC1 + s * HB) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, false, N2, &cs_res,
+               hp.fc1_b[s], CF::BF);
+    pack_block(img, (CF::O_FC2 + s * HB) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, false, N2, &cs_res,
+               hp.fc2_b[s], CF::BF);
+  }
+  for (int s = 1; s <= S; ++s)
+    pack_block(img, (CF::O_ATT + (s - 1) * tc::rup(CF::B_ATT, 128)) / 4, hp.att_W[s], NA, F, CF::FN, CF::KATT,
+               false, F, nullptr, hp.att_b[s], CF::BF);
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, CF::IMG_BYTES);
+  if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), CF::IMG_BYTES, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (d) cudaFree(d);
+    if (err) *err = cudaGetErrorString(e);
+    return false;
+  }
+  out->d_buf = d;
+  out->bytes = CF::IMG_BYTES;
+  out->params = new k2::Params{(const uint8_t*)d, (float)hp.gamma};
+  return true;
+}
+
+template <class CF>
+cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k2::tabnet_rowthread<CF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  k2::tabnet_rowthread<CF><<<grid, CF::THREADS, CF::SMEM_BYTES, stream>>>(*(const k2::Params*)m.params, a);
+  return cudaGetLastError();
+}
+
+#define TBN_K2(F, ND, NA, S, C, P)                                                  \
+  K2Instance{F, ND, NA, S, C, P, &pack_k2<k2::Cfg<F, ND, NA, S, C, P>>,            \
+             &launch_k2_impl<k2::Cfg<F, ND, NA, S, C, P>>}
+
+const K2Instance kK2[] = {
+    TBN_K2(14, 8, 8, 3, 2, tc::kPrecTF32),     // Adult
+    TBN_K2(14, 8, 8, 3, 2, tc::kPrecBF16),
+    TBN_K2(35, 16, 16, 5, 2, tc::kPrecTF32),   // HR
+    TBN_K2(35, 16, 16, 5, 2, tc::kPrecBF16),
+};
+
+const K2Instance* find_k2(const HostParams& hp, int precision) {
+  const int prec = precision == 1 ? tc::kPrecTF32 : precision == 2 ? tc::kPrecBF16 : -1;
+  for (const K2Instance& in : kK2)
+    if (in.F == hp.F && in.ND == hp.ND && in.NA == hp.NA && in.S == hp.S && in.C == hp.C && in.prec == prec)
+      return &in;
+  return nullptr;
+}
+
+}  // namespace
+
+bool k2_supported(const HostParams& hp, int precision) { return find_k2(hp, precision) != nullptr; }
+
+bool k2_pack(const HostParams& hp, int precision, TcModel* out, std::string* err) {
+  const K2Instance* in = find_k2(hp, precision);
+  if (!in) {
+    if (err) *err = "no K2 instance";
+    return false;
+  }
+  out->shape_id = (int)(in - kK2);
+  return in->pack(hp, out, err);
+}
+
+void k2_free(TcModel* m) {
+  if (m->d_buf) cudaFree(m->d_buf);
+  delete (k2::Params*)m->params;
+  m->d_buf = nullptr;
+  m->params = nullptr;
+}
+
+cudaError_t k2_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  if (m.shape_id < 0) return cudaErrorInvalidValue;
+  return kK2[m.shape_id].launch(m, a, num_sms, stream);
+}
+
+}  // namespace tbn

@@ -5,70 +5,18 @@
 // K-major in the UMMA canonical no-swizzle layout, split hi/lo for 3xTF32:
 // hi = rna_tf32(w), lo = rna_tf32(w - hi), both computed from the float64 weight.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "tbn_tc.h"
 #include "tc_kernel.cuh"
+#include "pack_util.h"
 
 namespace tbn {
 
 namespace {
 
-float tf32_rna_host(float x) {
-  uint32_t u;
-  std::memcpy(&u, &x, 4);
-  u = (u + 0x1000u) & 0xFFFFE000u;
-  float y;
-  std::memcpy(&y, &u, 4);
-  return y;
-}
-
-uint16_t bf16_rn_host(float x) {
-  uint32_t u;
-  std::memcpy(&u, &x, 4);
-  u += 0x7FFFu + ((u >> 16) & 1u);       // round to nearest even (finite inputs)
-  return (uint16_t)(u >> 16);
-}
-
-// bf16 variant: 16-bit elements, 8 per 16-byte core-matrix row:
-// element index (n/8)*(Kp*8) + (k/8)*64 + (n%8)*8 + (k%8).
-void pack_block_bf16(std::vector<float>& img, size_t off_floats, const double* W, int Kin, int Nvalid,
-                     int N, int Kp, int col_stride, const std::vector<double>* colscale,
-                     const double* bias) {
-  uint16_t* b = reinterpret_cast<uint16_t*>(img.data() + off_floats);
-  for (int n = 0; n < N; ++n)
-    for (int k = 0; k < Kp; ++k) {
-      const size_t idx = (size_t)(n / 8) * (Kp * 8) + (k / 8) * 64 + (n % 8) * 8 + (k % 8);
-      double w = (n < Nvalid && k < Kin) ? W[(size_t)k * col_stride + n] : 0.0;
-      if (bias && n < Nvalid && k == Kin) w = bias[n];
-      if (colscale) w *= (*colscale)[n];
-      b[idx] = bf16_rn_host((float)w);
-    }
-}
-
-// Pack W (Kin x N, row-major, x @ W) into B = W^T as N x Kp K-major canonical
-// blocks: float index (n/8)*(Kp*8) + (k/4)*32 + (n%8)*4 + (k%4).  Rows n >= Nvalid
-// and columns k >= Kin are zero.
-void pack_block(std::vector<float>& img, size_t off_floats, const double* W, int Kin, int Nvalid,
-                int N, int Kp, bool x3, int col_stride, const std::vector<double>* colscale = nullptr,
-                const double* bias = nullptr, bool bf16 = false) {
-  if (bf16) {
-    pack_block_bf16(img, off_floats, W, Kin, Nvalid, N, Kp, col_stride, colscale, bias);
-    return;
-  }
-  float* hi = img.data() + off_floats;
-  float* lo = hi + (size_t)N * Kp;
-  for (int n = 0; n < N; ++n)
-    for (int k = 0; k < Kp; ++k) {
-      const size_t idx = (size_t)(n / 8) * (Kp * 8) + (k / 4) * 32 + (n % 8) * 4 + (k % 4);
-      double w = (n < Nvalid && k < Kin) ? W[(size_t)k * col_stride + n] : 0.0;
-      if (bias && n < Nvalid && k == Kin) w = bias[n];     // bias row (ones column in A)
-      if (colscale) w *= (*colscale)[n];
-      float h = tf32_rna_host((float)w);
-      hi[idx] = h;
-      if (x3) lo[idx] = tf32_rna_host((float)(w - (double)h));
-    }
-}
+using pack::pack_block;
 
 struct Instance {
   int F, ND, NA, S, C, prec;
@@ -191,20 +139,39 @@ const Instance* find(const HostParams& hp, int precision) {
 
 }  // namespace
 
-bool tc_supported(const HostParams& hp, int precision) { return find(hp, precision) != nullptr; }
+bool tc_supported(const HostParams& hp, int precision) {
+  return k2_supported(hp, precision) || find(hp, precision) != nullptr;
+}
+
+// K2 (k2_kernel.cuh) serves the single-pass modes wherever an instance exists;
+// TBN_KERNEL=k1 pins the K1 design (development A/B only).
+static bool k2_allowed() {
+  const char* e = std::getenv("TBN_KERNEL");
+  return !(e && std::strcmp(e, "k1") == 0);
+}
 
 bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err) {
+  if (k2_allowed() && k2_supported(hp, precision)) {
+    out->kernel = 2;
+    out->precision = precision;
+    return k2_pack(hp, precision, out, err);
+  }
   const Instance* in = find(hp, precision);
   if (!in) {
     if (err) *err = "no instance";
     return false;
   }
+  out->kernel = 1;
   out->shape_id = (int)(in - kInstances);
   out->precision = precision;
   return in->pack(hp, out, err);
 }
 
 void tc_free(TcModel* m) {
+  if (m->kernel == 2) {
+    k2_free(m);
+    return;
+  }
   if (m->d_buf) cudaFree(m->d_buf);
   delete (tc::TcParams*)m->params;
   m->d_buf = nullptr;
@@ -212,6 +179,7 @@ void tc_free(TcModel* m) {
 }
 
 cudaError_t launch_tc(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  if (m.kernel == 2) return k2_launch(m, a, num_sms, stream);
   if (m.shape_id < 0) return cudaErrorInvalidValue;
   return kInstances[m.shape_id].launch(m, a, num_sms, stream);
 }

@@ -22,6 +22,7 @@ struct HostParams {
 };
 
 struct TcModel {
+  int kernel = 1;          // 1: K1 (tc_kernel.cuh), 2: K2 (k2_kernel.cuh)
   int shape_id = -1;       // which compiled instance
   int precision = 0;
   void* d_buf = nullptr;   // packed operands + epilogue constants
@@ -33,5 +34,11 @@ bool tc_supported(const HostParams& hp, int precision);
 bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
 void tc_free(TcModel* m);
 cudaError_t launch_tc(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream);
+
+// K2, the thread-per-row design for the single-pass modes (kernel_k2.cu)
+bool k2_supported(const HostParams& hp, int precision);
+bool k2_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
+void k2_free(TcModel* m);
+cudaError_t k2_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream);
 
 }  // namespace tbn

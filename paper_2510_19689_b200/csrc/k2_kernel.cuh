@@ -68,37 +68,55 @@ struct Cfg {
   static constexpr int DW = cmax(N2, FN);
   static constexpr int T_D = 0, T_A = DW, T_PR = DW + KA, T_END = T_PR + F;
   static constexpr int TCG = rup(T_END, 32);           // TMEM columns per group
-  // groups per CTA: TMEM and the register file (a row's live state is about
-  // 2F + H + 48 registers) both have to fit
-  static constexpr int REGS_ROW = 2 * F + H + 48;
   static constexpr int NG_TMEM = 512 / TCG;
-  static constexpr int NG_REG = 65536 / (128 * REGS_ROW);
-  static constexpr int NG = cmin(4, cmin(NG_TMEM, NG_REG));
+  // Register file: a row's live state is about 2F + H + 48 registers with xn
+  // in registers (variant R), F + H + 48 with xn in shared memory (variant S).
+  static constexpr int NG_R = cmin(4, cmin(NG_TMEM, 65536 / (128 * (2 * F + H + 48))));
+  static constexpr int NG_S = cmin(4, cmin(NG_TMEM, 65536 / (128 * (F + H + 48))));
+  // weight blocks (B operands, N x K K-major canonical)
+  static constexpr int B_SH1 = N2 * K1 * ESZ;
+  static constexpr int B_HID = N2 * KHID * ESZ;
+  static constexpr int B_ATT = FN * KATT * ESZ;
+  static constexpr int HBR = rup(B_HID, 128), ABR = rup(B_ATT, 128);
+  // consts (floats): scale F | shift F | head_W ND*C | head_b C
+  static constexpr int C_SCALE = 0, C_SHIFT = rup(F, 4), C_HW = C_SHIFT + rup(F, 4);
+  static constexpr int C_HB = C_HW + rup(ND * C, 4), C_END = rup(C_HB + C, 4);
+  static constexpr int CONST_BYTES = C_END * 4;
+  // global image: [consts][sh1][sh2][fc1_0..S][fc2_0..S][att_1..S], 128-B aligned blocks
+  static constexpr int O_SH1 = rup(CONST_BYTES, 128);
+  static constexpr int O_SH2 = O_SH1 + rup(B_SH1, 128);
+  static constexpr int O_FC1 = O_SH2 + HBR;
+  static constexpr int O_FC2 = O_FC1 + (S + 1) * HBR;
+  static constexpr int O_ATT = O_FC2 + (S + 1) * HBR;
+  static constexpr int IMG_BYTES = O_ATT + S * ABR;
+  static constexpr int STG = rup(32 * F * 4, 128);     // per-warp 32 x F row tile
+  static constexpr int SMEM_MAX = 227 * 1024 - 512;
+  // variant S (xn in SMEM, one more group): the fc1/fc2 blocks stream through a
+  // CTA-wide ring shared by the groups when the whole image does not fit
+  static constexpr int FIX_S = O_FC1 + S * ABR;        // consts, sh1, sh2, att resident
+  static constexpr int STG_S = 2 * (NG_S * 4) * STG;
+  static constexpr bool S_RES = IMG_BYTES + STG_S <= SMEM_MAX;
+  static constexpr int S_SLOTS = cmin(6, (SMEM_MAX - FIX_S - STG_S) / HBR);
+  static constexpr bool S_OK = NG_S > NG_R && (S_RES || S_SLOTS >= 3);
+  static constexpr bool XS = S_OK;                     // xn in shared memory
+  static constexpr int NG = XS ? NG_S : NG_R;
+  static constexpr bool RING = XS && !S_RES;
+  static constexpr int NSLOT = RING ? S_SLOTS : 0;
+  static constexpr int NB = 2 * (S + 1);               // ring blocks per tile: fc1_s, fc2_s
   static_assert(NG >= 1, "per-row state does not fit");
   static constexpr int TCOLS = pow2ceil(NG * TCG);
   static_assert(TCOLS <= 512, "TMEM");
   static_assert(N2 <= 256 && FN <= 256, "MMA N > 256");
   static constexpr int THREADS = NG * 128;
   static constexpr int NW = NG * 4;
-  // weight blocks (B operands, N x K K-major canonical)
-  static constexpr int B_SH1 = N2 * K1 * ESZ;
-  static constexpr int B_HID = N2 * KHID * ESZ;
-  static constexpr int B_ATT = FN * KATT * ESZ;
-  // consts (floats): scale F | shift F | head_W ND*C | head_b C
-  static constexpr int C_SCALE = 0, C_SHIFT = rup(F, 4), C_HW = C_SHIFT + rup(F, 4);
-  static constexpr int C_HB = C_HW + rup(ND * C, 4), C_END = rup(C_HB + C, 4);
-  static constexpr int CONST_BYTES = C_END * 4;
-  // image: [consts][sh1][sh2][fc1_0..S][fc2_0..S][att_1..S], 128-B aligned blocks
-  static constexpr int O_SH1 = rup(CONST_BYTES, 128);
-  static constexpr int O_SH2 = O_SH1 + rup(B_SH1, 128);
-  static constexpr int O_FC1 = O_SH2 + rup(B_HID, 128);
-  static constexpr int O_FC2 = O_FC1 + (S + 1) * rup(B_HID, 128);
-  static constexpr int O_ATT = O_FC2 + (S + 1) * rup(B_HID, 128);
-  static constexpr int IMG_BYTES = O_ATT + S * rup(B_ATT, 128);
-  static constexpr int STG = rup(32 * F * 4, 128);     // per-warp row staging
-  static constexpr int OFF_STG = rup(IMG_BYTES, 1024);
-  static constexpr int OFF_BAR = OFF_STG + NW * STG;
-  static constexpr int SMEM_BYTES = OFF_BAR + 256;
+  // shared-memory plan: resident image (or its fixed part + att + ring) | staging | bars
+  static constexpr int S_ATT = RING ? O_FC1 : O_ATT;   // where att_1 lives in SMEM
+  static constexpr int OFF_RING = O_FC1 + S * ABR;
+  static constexpr int RES_BYTES = RING ? OFF_RING + NSLOT * HBR : IMG_BYTES;
+  static constexpr int OFF_STG = rup(RES_BYTES, 1024);
+  static constexpr int OFF_XS = OFF_STG + NW * STG;    // variant S: per-warp xn tiles
+  static constexpr int OFF_BAR = OFF_XS + (XS ? NW * STG : 0);
+  static constexpr int SMEM_BYTES = OFF_BAR + 512;
   static_assert(SMEM_BYTES <= 227 * 1024, "weights + staging exceed shared memory");
 };
 
@@ -111,6 +129,8 @@ struct Bars {
   uint64_t cfull;
   uint64_t dfull[4];       // per group: MMA chain complete
   uint64_t xfull[16];      // per warp: x row tile landed
+  uint64_t rfull[8];       // ring slots (variant S, streamed fc1/fc2 blocks)
+  uint32_t rcnt[8];        // ring slots: monotonic release counters
   uint32_t tmem_base;
 };
 
@@ -151,6 +171,7 @@ __global__ void __launch_bounds__(CF::THREADS, 1)
 tabnet_rowthread(const Params p, const ForwardArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int F = CF::F, H = CF::H, ND = CF::ND, NA = CF::NA, S = CF::S, C = CF::C, NG = CF::NG;
+  constexpr int NB = CF::NB, NSLOT = CF::NSLOT;
   const float* cst = reinterpret_cast<const float*>(smem);
   Bars* bars = reinterpret_cast<Bars*>(smem + CF::OFF_BAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,17 +179,48 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   const int t = q * 32 + lane;                      // row within the tile == TMEM lane
   const int64_t ntiles = (a.rows + 127) / 128;
   const bool x_bulk_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0);
+  // this CTA's tiles: blockIdx.x + gridDim.x * m, m = g + NG * round
+  const int64_t tiles_cta = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t rounds = (tiles_cta + NG - 1) / NG;
+  const uint32_t nblk = (uint32_t)(rounds * NB);    // ring blocks this CTA streams
+
+  // ring block v (variant S): fc1_s / fc2_s of tile round v / NB, s = (v % NB) / 2
+  auto ring_src = [&](uint32_t v) -> const uint8_t* {
+    const uint32_t i = v % NB;
+    return p.wimg + ((i & 1) ? CF::O_FC2 : CF::O_FC1) + (i >> 1) * CF::HBR;
+  };
+  auto ring_load = [&](uint32_t v) {
+    const int sl = (int)(v % NSLOT);
+    ptx::mbar_arrive_expect_tx(&bars->rfull[sl], CF::B_HID);
+    ptx::bulk_g2s(smem + CF::OFF_RING + sl * CF::HBR, ring_src(v), CF::B_HID, &bars->rfull[sl]);
+  };
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bars->cfull, 1);
     for (int i = 0; i < NG; ++i) ptx::mbar_init(&bars->dfull[i], 1);
     for (int i = 0; i < CF::NW; ++i) ptx::mbar_init(&bars->xfull[i], 1);
+    for (int i = 0; i < NSLOT; ++i) {
+      ptx::mbar_init(&bars->rfull[i], 1);
+      bars->rcnt[i] = 0;
+    }
     ptx::fence_mbar_init();
-    ptx::mbar_arrive_expect_tx(&bars->cfull, CF::IMG_BYTES);
     constexpr int CH = 32768;
-    for (int o = 0; o < CF::IMG_BYTES; o += CH)
-      ptx::bulk_g2s(smem + o, p.wimg + o, (uint32_t)(CF::IMG_BYTES - o < CH ? CF::IMG_BYTES - o : CH),
-                    &bars->cfull);
+    if constexpr (!CF::RING) {
+      ptx::mbar_arrive_expect_tx(&bars->cfull, CF::IMG_BYTES);
+      for (int o = 0; o < CF::IMG_BYTES; o += CH)
+        ptx::bulk_g2s(smem + o, p.wimg + o, (uint32_t)(CF::IMG_BYTES - o < CH ? CF::IMG_BYTES - o : CH),
+                      &bars->cfull);
+    } else {
+      // consts + sh1 + sh2 (image prefix), then the attentive blocks behind them
+      constexpr int ATT_BYTES = S * CF::ABR;
+      ptx::mbar_arrive_expect_tx(&bars->cfull, CF::O_FC1 + ATT_BYTES);
+      for (int o = 0; o < CF::O_FC1; o += CH)
+        ptx::bulk_g2s(smem + o, p.wimg + o, (uint32_t)(CF::O_FC1 - o < CH ? CF::O_FC1 - o : CH), &bars->cfull);
+      for (int o = 0; o < ATT_BYTES; o += CH)
+        ptx::bulk_g2s(smem + CF::S_ATT + o, p.wimg + CF::O_ATT + o,
+                      (uint32_t)(ATT_BYTES - o < CH ? ATT_BYTES - o : CH), &bars->cfull);
+      for (uint32_t v = 0; v < (uint32_t)NSLOT && v < nblk; ++v) ring_load(v);
+    }
   }
   if (warp == 0) ptx::tmem_alloc<CF::TCOLS>(&bars->tmem_base);
   ptx::tc_fence_before();
@@ -177,22 +229,24 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   const uint32_t tg = bars->tmem_base + (uint32_t)(g * CF::TCG) + ((uint32_t)(q * 32) << 16);
   const uint32_t tD = tg + CF::T_D, tA = tg + CF::T_A, tPR = tg + CF::T_PR;
   float* stg = reinterpret_cast<float*>(smem + CF::OFF_STG + warp * CF::STG);
+  // where x lands and xn lives: its own per-warp tile (variant S) or the staging tile
+  float* xst = CF::XS ? reinterpret_cast<float*>(smem + CF::OFF_XS + warp * CF::STG) : stg;
   const uint32_t bar_id = 1 + g;
   uint32_t dphase = 0, xphase = 0;
 
-  // stage this warp's rows [r0w, r0w + nw) of x into stg (TMA bulk + tail)
+  // stage this warp's rows [r0w, r0w + nw) of x into xst (TMA bulk + tail)
   auto load_x = [&](int64_t r0w, int nw) {
     const int ne = nw * F;
     const int nb = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
     if (lane == 0) {
       if (nb > 0) {
         ptx::mbar_arrive_expect_tx(&bars->xfull[warp], (uint32_t)nb * 4u);
-        ptx::bulk_g2s(stg, a.x + r0w * F, (uint32_t)nb * 4u, &bars->xfull[warp]);
+        ptx::bulk_g2s(xst, a.x + r0w * F, (uint32_t)nb * 4u, &bars->xfull[warp]);
       } else {
         ptx::mbar_arrive(&bars->xfull[warp]);
       }
     }
-    for (int e = nb + lane; e < 32 * F; e += 32) stg[e] = e < ne ? __ldg(a.x + r0w * F + e) : 0.0f;
+    for (int e = nb + lane; e < 32 * F; e += 32) xst[e] = e < ne ? __ldg(a.x + r0w * F + e) : 0.0f;
     ptx::mbar_wait(&bars->xfull[warp], xphase);
     xphase ^= 1;
     __syncwarp();
@@ -214,6 +268,14 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     if (lane == 0) ptx::bulk_wait_read0();
     __syncwarp();
   };
+  // ring block v no longer needed by this group: the last of the NG groups to
+  // release it refills its slot with block v + NSLOT.  Counters are monotonic:
+  // use u = v / NSLOT of a slot completes at arrival (u + 1) * NG.
+  auto ring_release = [&](uint32_t v) {
+    const uint32_t sl = v % NSLOT;
+    const uint32_t old = atomicAdd(&bars->rcnt[sl], 1u);
+    if (old == (v / NSLOT) * NG + NG - 1 && v + NSLOT < nblk) ring_load(v + NSLOT);
+  };
 
   ptx::mbar_wait(&bars->cfull, 0);
   if (a.scale) {     // batch-statistics control: override the affine in this CTA's copy
@@ -226,12 +288,12 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   __syncthreads();
 
   const uint32_t wbase = ptx::smem_u32(smem);
-  // One GEMM: A (this group's TMEM) x B (resident block at byte offset bo).
-  // The group meets at its barrier, warp 0 of the group issues the chain and
-  // commits it; `post` overlaps the MMA; then everyone waits for D.
+  // One GEMM: A (this group's TMEM) x B (SMEM block at byte offset bo, or ring
+  // block rv).  The group meets at its barrier, warp 0 of the group issues the
+  // chain and commits it; `post` overlaps the MMA; then everyone waits for D.
   int jt = 0;                                    // trace: GEMM counter
   const bool tr = (q == 0 && lane == 0);
-  auto gemm = [&](int kind, uint32_t bo, auto&& post) {
+  auto gemm = [&](int kind, uint32_t bo, int64_t rv, auto&& post) {
     if (tr) TBN_TRACE(g * 4000 + 4 * jt);
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
@@ -239,6 +301,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 1);
     if (q == 0) {
       ptx::tc_fence_after();
+      if constexpr (CF::RING) {
+        if (rv >= 0) {
+          const uint32_t v = (uint32_t)rv;
+          ptx::mbar_wait(&bars->rfull[v % NSLOT], (v / NSLOT) & 1u);
+          bo = CF::OFF_RING + (v % NSLOT) * CF::HBR;
+        }
+      }
       if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tA, wbase + bo);
       else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tA, wbase + bo);
       else tc::issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tA, wbase + bo);
@@ -249,16 +318,23 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     ptx::mbar_wait(&bars->dfull[g], dphase);
     dphase ^= 1;
     ptx::tc_fence_after();
+    if constexpr (CF::RING) {
+      if (rv >= 0 && tr) ring_release((uint32_t)rv);
+    }
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 3);
     ++jt;
   };
   auto nopost = [] {};
 
-  float xn[F], agg[F], gv[H], lacc[C];
+  float xnr[CF::XS ? 1 : F], agg[F], gv[H], lacc[C];
+  auto xn_at = [&](int f) -> float {
+    if constexpr (CF::XS) return xst[lane * F + f];
+    else return xnr[f];
+  };
 
   // GLU block over D = [lin' | gate'] (H + H columns): gv <- lin'(1+t) [+ R gv]
   auto glu = [&](bool residual) {
-    constexpr int CW = H < 16 ? H : 16;
+    constexpr int CW = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);
     static_assert(H % CW == 0, "GLU chunking");
     float lin[CW], gate[CW];
     tmem_load_n<CW>(tD, lin);
@@ -290,15 +366,29 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   };
   auto store_g = [&]() { put_a<CF, 0, H>(tA, gv); };
 
-  for (int64_t k = 0;; ++k) {
-    const int64_t tile = (int64_t)blockIdx.x + (int64_t)gridDim.x * (g + (int64_t)NG * k);
-    if (tile >= ntiles) break;
+  for (int64_t k = 0; k < rounds; ++k) {
+    const int64_t m = g + (int64_t)NG * k;
+    if (m >= tiles_cta) {
+      // no tile for this group in the last round: release its ring blocks
+      if constexpr (CF::RING) {
+        if (tr) {
+          for (uint32_t i = 0; i < (uint32_t)NB; ++i) {
+            const uint32_t v = (uint32_t)(k * NB) + i;
+            ptx::mbar_wait(&bars->rfull[v % NSLOT], (v / NSLOT) & 1u);
+            ring_release(v);
+          }
+        }
+      }
+      break;
+    }
+    const int64_t tile = (int64_t)blockIdx.x + (int64_t)gridDim.x * m;
     const int64_t r0 = tile * 128;
     const int nrows = (int)(a.rows - r0 < 128 ? a.rows - r0 : 128);
     const int nw = nrows - q * 32 < 0 ? 0 : (nrows - q * 32 > 32 ? 32 : nrows - q * 32);
     const bool valid = lane < nw;
     const int64_t row = r0 + t;
     const int64_t r0w = r0 + q * 32;
+    const int64_t rv0 = CF::RING ? k * NB : -1;     // this tile's first ring block
 
     // ---- x -> xn (network.py:118-120), prior = 1, agg = 0 ----
     if (tr) TBN_TRACE(g * 4000 + 3000 + 8 * (int)k);
@@ -309,23 +399,37 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     if (tr) TBN_TRACE(g * 4000 + 3001 + 8 * (int)k);
     {
       int bad = 0;
+      float xv[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) {
-        const float xv = nw > 0 ? stg[lane * F + f] : 0.0f;
-        bad |= !isfinite(xv);
-        const float sh = a.normalized ? 0.0f : cst[CF::C_SHIFT + f];
-        const float sc = a.normalized ? 1.0f : cst[CF::C_SCALE + f];
-        xn[f] = (xv - sh) * sc;
+        xv[f] = nw > 0 ? xst[lane * F + f] : 0.0f;
+        bad |= !isfinite(xv[f]);
         agg[f] = 0.0f;
       }
+      if (!a.normalized) {        // (x - mean) * rsqrt(var + eps), pairwise
+#pragma unroll
+        for (int f = 0; f + 1 < F; f += 2) {
+          const float2 v = __fmul2_rn(__fadd2_rn(f2(xv[f], xv[f + 1]),
+                                                 f2(-cst[CF::C_SHIFT + f], -cst[CF::C_SHIFT + f + 1])),
+                                      f2(cst[CF::C_SCALE + f], cst[CF::C_SCALE + f + 1]));
+          xv[f] = v.x;
+          xv[f + 1] = v.y;
+        }
+        if constexpr (F % 2) xv[F - 1] = (xv[F - 1] - cst[CF::C_SHIFT + F - 1]) * cst[CF::C_SCALE + F - 1];
+      }
       if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        if constexpr (CF::XS) xst[lane * F + f] = xv[f];
+        else xnr[f] = xv[f];
+      }
       float one[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) one[f] = 1.0f;
       tmem_store_n<F>(tPR, one);
       float av[CF::K1];
 #pragma unroll
-      for (int e = 0; e < CF::K1; ++e) av[e] = e < F ? xn[e] : (e == F ? 1.0f : 0.0f);
+      for (int e = 0; e < CF::K1; ++e) av[e] = e < F ? xv[e] : (e == F ? 1.0f : 0.0f);
       put_a<CF, 0, CF::K1>(tA, av);
     }
 #pragma unroll
@@ -334,19 +438,19 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
 
     // feature transformer (network.py:124-141)
     auto transform = [&](int s, auto&& post_first) {
-      const uint32_t o1 = CF::O_FC1 + (uint32_t)s * rup(CF::B_HID, 128);
-      const uint32_t o2 = CF::O_FC2 + (uint32_t)s * rup(CF::B_HID, 128);
-      gemm(0, CF::O_SH1, post_first);
+      const uint32_t o1 = CF::O_FC1 + (uint32_t)s * CF::HBR;
+      const uint32_t o2 = CF::O_FC2 + (uint32_t)s * CF::HBR;
+      gemm(0, CF::O_SH1, -1, post_first);
       glu(false);
       store_g();
       put_ones<CF, H, CF::KHID - H>(tA);        // hidden-GEMM bias column
-      gemm(1, CF::O_SH2, nopost);
+      gemm(1, CF::O_SH2, -1, nopost);
       glu(true);
       store_g();
-      gemm(1, o1, nopost);
+      gemm(1, o1, CF::RING ? rv0 + 2 * s : -1, nopost);
       glu(true);
       store_g();
-      gemm(1, o2, nopost);
+      gemm(1, o2, CF::RING ? rv0 + 2 * s + 1 : -1, nopost);
       glu(true);
     };
     // d = relu(f[:, :n_d]); eta = sum d; logits accumulate (the head is linear,
@@ -356,8 +460,18 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
 #pragma unroll
       for (int i = 0; i < ND; ++i) {
         const float d = fmaxf(gv[i], 0.0f);
+        if constexpr (C % 2 == 0) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) lacc[c] = fmaf(d, cst[CF::C_HW + i * C + c], lacc[c]);
+          for (int c = 0; c < C; c += 2) {
+            const float2 v = __ffma2_rn(f2(d, d), f2(cst[CF::C_HW + i * C + c], cst[CF::C_HW + i * C + c + 1]),
+                                        f2(lacc[c], lacc[c + 1]));
+            lacc[c] = v.x;
+            lacc[c + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c) lacc[c] = fmaf(d, cst[CF::C_HW + i * C + c], lacc[c]);
+        }
         if (i & 1) e1 += d; else e0 += d;
       }
       return e0 + e1;
@@ -369,8 +483,12 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       const bool reset = all_eta_zero && eta > 0.0f;
       const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
       all_eta_zero = all_eta_zero && !(eta > 0.0f);
+      if (reset) {              // rare: only rows whose earlier steps all had eta == 0
 #pragma unroll
-      for (int f = 0; f < F; ++f) agg[f] = fmaf(w, stg[lane * F + f], reset ? 0.0f : agg[f]);
+        for (int f = 0; f < F; ++f) agg[f] = 0.0f;
+      }
+#pragma unroll
+      for (int f = 0; f < F; ++f) agg[f] = fmaf(w, stg[lane * F + f], agg[f]);
     };
 
     transform(0, nopost);                                        // network.py:226-227
@@ -385,7 +503,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         if (s > 1) eta_prev = step_eta();
         put_a<CF, 0, CF::KATT>(tA, av);
       }
-      gemm(2, CF::O_ATT + (uint32_t)(s - 1) * rup(CF::B_ATT, 128), [&] {
+      gemm(2, CF::S_ATT + (uint32_t)(s - 1) * CF::ABR, -1, [&] {
         if (s > 1) agg_apply(eta_prev);
       });
       // attentive transformer + sparsemax (network.py:233-238, sparsemax.py:13-41)
@@ -396,21 +514,37 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         tmem_load_n<F>(tPR, pr);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < F; ++i) z[i] = pr[i] * z[i];           // bias already in D
+        for (int i = 0; i + 1 < F; i += 2) {                       // bias already in D
+          const float2 v = __fmul2_rn(f2(pr[i], pr[i + 1]), f2(z[i], z[i + 1]));
+          z[i] = v.x;
+          z[i + 1] = v.y;
+        }
+        if constexpr (F % 2) z[F - 1] = pr[F - 1] * z[F - 1];
       }
       float zmax, tau;
       if (tr) TBN_TRACE(g * 4000 + 3500 + 4 * s);
       {
-        float m0 = -INFINITY, m1 = -INFINITY, s0 = 0.0f, s1 = 0.0f;
+        float m0 = -INFINITY, m1 = -INFINITY;
+        float2 s2 = f2(0.0f, 0.0f);
 #pragma unroll
-        for (int i = 0; i < F; ++i) {
-          if (i & 1) { m1 = fmaxf(m1, z[i]); s1 += z[i]; }
-          else { m0 = fmaxf(m0, z[i]); s0 += z[i]; }
+        for (int i = 0; i + 1 < F; i += 2) {
+          m0 = fmaxf(m0, z[i]);
+          m1 = fmaxf(m1, z[i + 1]);
+          s2 = __fadd2_rn(s2, f2(z[i], z[i + 1]));
+        }
+        if constexpr (F % 2) {
+          m0 = fmaxf(m0, z[F - 1]);
+          s2.x += z[F - 1];
         }
         zmax = fmaxf(m0, m1);
-        const float zsum = s0 + s1;
+        const float zsum = s2.x + s2.y;
 #pragma unroll
-        for (int i = 0; i < F; ++i) z[i] -= zmax;                  // sparsemax.py:32
+        for (int i = 0; i + 1 < F; i += 2) {                        // sparsemax.py:32
+          const float2 v = __fadd2_rn(f2(z[i], z[i + 1]), f2(-zmax, -zmax));
+          z[i] = v.x;
+          z[i + 1] = v.y;
+        }
+        if constexpr (F % 2) z[F - 1] -= zmax;
         // tau: Michelot's fixed point tau <- (sum_{z>tau} z - 1)/|{z > tau}|, monotone
         // from a lower bound; its support equals the reference's sort/cumsum/count
         // k (sparsemax.py:33-39).  Start: max(-1, (sum z - 1)/F) nudged down 2^-20.
@@ -421,46 +555,71 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
           float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
 #pragma unroll
           for (int i = 0; i + 1 < F; i += 2) {
-            const float2 m = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
+            const float2 mk = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
             if ((i / 2) % 2 == 0) {
-              sa = __ffma2_rn(m, f2(z[i], z[i + 1]), sa);
-              ca = __fadd2_rn(ca, m);
+              sa = __ffma2_rn(mk, f2(z[i], z[i + 1]), sa);
+              ca = __fadd2_rn(ca, mk);
             } else {
-              sb = __ffma2_rn(m, f2(z[i], z[i + 1]), sb);
-              cb = __fadd2_rn(cb, m);
+              sb = __ffma2_rn(mk, f2(z[i], z[i + 1]), sb);
+              cb = __fadd2_rn(cb, mk);
             }
           }
           const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
           float sm = s2.x + s2.y, cn = c2.x + c2.y;
           if constexpr (F % 2) {
-            const float m = z[F - 1] > tau ? 1.0f : 0.0f;
-            sm = fmaf(m, z[F - 1], sm);
-            cn += m;
+            const float mk = z[F - 1] > tau ? 1.0f : 0.0f;
+            sm = fmaf(mk, z[F - 1], sm);
+            cn += mk;
           }
           if (cn >= cnt_prev) break;
           cnt_prev = cn;
           tau = __fdividef(sm - 1.0f, cn);                            // sparsemax.py:39
         }
       }
-      // mask, prior update, x*mask -> A; mask -> staging (network.py:236-238, :246)
+      // mask, prior update, x*mask -> A; mask -> staging (network.py:236-238, :246),
+      // in 16-feature chunks (A chunks of the shared1 K layout)
       if (tr) TBN_TRACE(g * 4000 + 3501 + 4 * s);
       claim_stg();
       {
-        float pr[F];
-        tmem_load_n<F>(tPR, pr);
-        ptx::tmem_ld_wait();
-        float av[CF::K1];
+        const float2 gm2 = f2(p.gamma, p.gamma), nt2 = f2(-tau, -tau);
+        chunked<CF::K1, 16>([&](auto o, auto l) {
+          constexpr int O = decltype(o)::value, L = decltype(l)::value;
+          constexpr int LF = (O + L <= F) ? L : (O < F ? F - O : 0);   // features in this chunk
+          float pr[LF > 0 ? LF : 1], av[L];
+          if constexpr (LF > 0) {
+            tmem_load_n<LF>(tPR + O, pr);
+            ptx::tmem_ld_wait();
+          }
 #pragma unroll
-        for (int f = 0; f < F; ++f) {
-          const float m = fmaxf(z[f] - tau, 0.0f);                   // sparsemax.py:40
-          pr[f] = pr[f] * (p.gamma - m);                             // network.py:237
-          av[f] = m * xn[f];                                         // network.py:238
-          stg[lane * F + f] = m;
-        }
+          for (int i = 0; i < L; i += 2) {
+            const int f = O + i;
+            if (f + 1 < F) {
+              const float2 d = __fadd2_rn(f2(z[f], z[f + 1]), nt2);
+              const float2 mk = f2(fmaxf(d.x, 0.0f), fmaxf(d.y, 0.0f));      // sparsemax.py:40
+              const float2 np = __fmul2_rn(f2(pr[i], pr[i + 1]), __fadd2_rn(gm2, f2(-mk.x, -mk.y)));  // :237
+              const float2 xm = __fmul2_rn(mk, f2(xn_at(f), xn_at(f + 1)));    // network.py:238
+              pr[i] = np.x; pr[i + 1] = np.y;
+              av[i] = xm.x; av[i + 1] = xm.y;
+              stg[lane * F + f] = mk.x;
+              stg[lane * F + f + 1] = mk.y;
+            } else {
 #pragma unroll
-        for (int e = F; e < CF::K1; ++e) av[e] = e == F ? 1.0f : 0.0f;
-        tmem_store_n<F>(tPR, pr);
-        put_a<CF, 0, CF::K1>(tA, av);
+              for (int u = 0; u < 2; ++u) {
+                const int fu = f + u;
+                if (fu < F) {
+                  const float mk = fmaxf(z[fu] - tau, 0.0f);
+                  pr[i + u] = pr[i + u] * (p.gamma - mk);
+                  av[i + u] = mk * xn_at(fu);
+                  stg[lane * F + fu] = mk;
+                } else {
+                  av[i + u] = fu == F ? 1.0f : 0.0f;                      // ones column (bias row)
+                }
+              }
+            }
+          }
+          if constexpr (LF > 0) tmem_store_n<LF>(tPR + O, pr);
+          put_a<CF, O, L>(tA, av);
+        });
       }
       // masks[s-1] of this warp's rows leave while the shared1 MMA runs
       transform(s, [&] {

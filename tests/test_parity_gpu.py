@@ -19,6 +19,9 @@ pytestmark = pytest.mark.gpu
 
 # precisions with a compiled kernel, and the bound each is held to
 EXACT_PRECISIONS = ["fp32", "tf32x3"]
+# every GPU mode (incl. the single-pass ones held to stated looser bounds): the
+# contracts that do not depend on precision (invariance, errors, API objects)
+ALL_PRECISIONS = ["fp32", "tf32x3", "tf32", "bf16"]
 CASES = [f"{n}_{r}" for n in ("adult", "hr", "bls", "wide") for r in ("init", "trained")]
 TC_SHAPES = ("adult", "hr", "bls")       # shapes with a compiled tcgen05 instance
 _NAMES = {"adult": "adult", "hr": "hr", "bls": "bls", "wide": "wide"}
@@ -128,7 +131,7 @@ def load_invariance_check(model, x, concurrency=(1, 32), batch_sizes=(1, 256), u
     return True
 
 
-@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+@pytest.mark.parametrize("precision", ALL_PRECISIONS)
 def test_load_invariance_bitwise(precision):
     m = P.TabNetModel.from_reference(W.make_model("hr"), precision=precision)
     x = W.make_inputs(W.WORKLOADS["hr"], 512).astype(np.float64)
@@ -137,7 +140,7 @@ def test_load_invariance_bitwise(precision):
     assert not load_invariance_check(m, x, use_batch_stats=True)
 
 
-@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+@pytest.mark.parametrize("precision", ALL_PRECISIONS)
 def test_nonfinite_and_width_errors(precision):
     m = P.TabNetModel.from_reference(W.make_model("adult"), precision=precision)
     x = np.zeros((300, 14))
@@ -177,7 +180,7 @@ def test_attentive_step_spec():
     np.testing.assert_allclose(new_prior, [[0, 1, 1]], atol=1e-7)
 
 
-@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+@pytest.mark.parametrize("precision", ALL_PRECISIONS)
 def test_forward_objects(precision):
     m = P.TabNetModel.from_reference(W.make_model("adult"), precision=precision)
     x = W.make_inputs(W.WORKLOADS["adult"], 33).astype(np.float64)
@@ -189,7 +192,7 @@ def test_forward_objects(precision):
         assert np.array_equal(o.explanation.step_masks, r.masks[:, i, :])
 
 
-@pytest.mark.parametrize("precision", EXACT_PRECISIONS)
+@pytest.mark.parametrize("precision", ALL_PRECISIONS)
 def test_shard_and_device_path_bitwise(precision):
     """Row shards processed as separate calls (as 1/2/4/8 GPUs would) and the
     zero-copy torch device path are bitwise equal to one full call."""

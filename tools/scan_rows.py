@@ -9,10 +9,10 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "hr"
 for prec in sys.argv[2:] or ["tf32x3", "tf32"]:
     w = W.WORKLOADS[cfg]
     m = TabNetModel.from_reference(W.make_model(cfg, "trained"), precision=prec, device=0)
-    maxr = 148 * 256 * 4
+    maxr = 148 * 128 * 16
     r = DeviceRunner(m, maxr, device=0)
     x = torch.from_numpy(W.make_inputs(w, maxr)).cuda()
-    for rows in (128, 148 * 256, 65536, 148 * 1024):
+    for rows in [int(v) for v in __import__('os').environ.get('ROWS', '128,37888,56832,65536,151552').split(',')]:
         xs = x[:rows].contiguous()
         for _ in range(3):
             r.run(xs)

@@ -43,11 +43,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="hr", choices=sorted(W.WORKLOADS))
     ap.add_argument("--rows", type=int, default=0, help="rows per rank (default: the config's batch)")
-    ap.add_argument("--precision", default="tf32x3")
+    ap.add_argument("--precision", default="bf16",
+                    choices=["bf16", "tf32", "tf32x3", "fp32"],
+                    help="FC contraction arithmetic (bf16: the production mode; tf32x3: the "
+                         "fp32-faithful exactness mode)")
     ap.add_argument("--regime", default="trained", choices=["trained", "init"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch each timed step from Python instead of replaying a CUDA graph")
     ap.add_argument("--latency-sweep", action="store_true",
                     help="also report p50/p99 device+e2e latency for batches 1..1024 (config 3)")
     return ap.parse_args()
@@ -203,6 +208,41 @@ def profile_traffic(config: str, precision: str):
         return None
 
 
+def roofline(precision: str, counts: dict, rows: int, kernel_ms: float, peaks: dict) -> dict:
+    """t_roof = max(bytes / HBM, flops * passes / P_mode); the
+    binding roof is reported (achieved and peak in its units), the other one
+    alongside.  passes = 3 for 3xTF32 (three MMAs per product), else 1."""
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    tf32_file = ROOT / "profiles" / "measured_tf32.json"
+    tf32 = json.loads(tf32_file.read_text()) if tf32_file.exists() else {}
+    if precision == "bf16":
+        tpk, tsrc = peaks.get("bf16_tflops", 2250.0), "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst)"
+    elif precision in ("tf32", "tf32x3"):
+        tpk = tf32.get("tf32_tflops", peaks.get("bf16_tflops", 2250.0) / 2)
+        tsrc = ("profiles/measured_tf32.json tf32_tflops (cuBLAS fp32+allow_tf32 8192^3, burst)"
+                if tf32 else "estimate: MEASURED_PEAKS bf16_tflops / 2")
+    else:
+        tpk, tsrc = None, "no tensor-core path (CUDA-core fp32)"
+    passes = 3 if precision == "tf32x3" else 1
+    t_s = kernel_ms / 1e3
+    bytes_ = counts["bytes_per_row"] * rows
+    flops = counts["flops_per_row"] * rows * passes
+    t_hbm = bytes_ / (hbm * 1e9)
+    t_ten = flops / (tpk * 1e12) if tpk else 0.0
+    hbm_part = {"achieved": bytes_ / t_s / 1e9, "peak": hbm, "unit": "GB/s", "frac": t_hbm / t_s}
+    ten_part = ({"achieved": flops / t_s / 1e12, "peak": tpk, "unit": "TFLOP/s", "frac": t_ten / t_s,
+                 "passes": passes, "peak_source": tsrc} if tpk else None)
+    bound = "tensor" if (tpk and t_ten > t_hbm) else "hbm"
+    main = ten_part if bound == "tensor" else hbm_part
+    return {"bound": bound, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
+            "frac": main["frac"], "traffic": None,
+            "hbm": hbm_part, "tensor": ten_part,
+            "algorithmic_bytes_per_row": counts["bytes_per_row"],
+            "algorithmic_flops_per_row": counts["flops_per_row"],
+            "kernel_ms_per_launch": kernel_ms,
+            "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650 GB/s"}
+
+
 def run_ours(a) -> None:
     import torch
     import torch.distributed as dist
@@ -235,6 +275,28 @@ def run_ours(a) -> None:
         runner.run(xs[i % nsets], outs[i % nsets])
     torch.cuda.synchronize()
     runner.check_finite()
+    # One CUDA graph per rotating set, each holding that step's single fused
+    # launch: the timed loop replays them, so host launch overhead (ctypes +
+    # Python, tens of us) never leaves the GPU idle between steps.
+    step_fns = [(lambda i=i: runner.run(xs[i], outs[i], stream=torch.cuda.current_stream(dev)))
+                for i in range(nsets)]
+    if not a.no_graph:
+        graphs = []
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            for i in range(nsets):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    runner.run(xs[i], outs[i], stream=side)
+                graphs.append(g)
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        step_fns = [g.replay for g in graphs]
+        for i in range(nsets):
+            step_fns[i]()
+        torch.cuda.synchronize()
+        runner.check_finite()
 
     clocks = ClockSampler(local)
     if world > 1:
@@ -245,7 +307,7 @@ def run_ours(a) -> None:
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
     ev[0].record(stream)
     for i in range(a.steps):
-        runner.run(xs[i % nsets], outs[i % nsets])
+        step_fns[i % nsets]()
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -306,10 +368,8 @@ def run_ours(a) -> None:
                          f"oracle/tabnet_oracle.py (bitwise = reference apply) on {procs} processes"}
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = counts["bytes_per_row"] * rows / (kernel_ms / 1e3) / 1e9
-    tflops = counts["flops_per_row"] * rows / (kernel_ms / 1e3) / 1e12
-    traffic = profile_traffic(a.config, a.precision)
+    roof = roofline(a.precision, counts, rows, kernel_ms, peaks)
+    roof["traffic"] = profile_traffic(a.config, a.precision)
     if rank == 0:
         line = {
             "metric": "TabNet inferences/sec (predict+explain)",
@@ -321,14 +381,9 @@ def run_ours(a) -> None:
             "config": {"workload": w.description, "rows_per_rank": rows, "regime": a.regime,
                        "precision": a.precision, "outputs": "logits, probabilities, masks (S,B,F), importance, class",
                        "parallelism": f"row-shard x{world} (no collective)",
-                       "l2": f"rotating {nsets} input/output sets = {nsets * per_set / 2**20:.0f} MiB > 126 MiB L2"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
-                         "algorithmic_bytes_per_row": counts["bytes_per_row"],
-                         "algorithmic_flops_per_row": counts["flops_per_row"],
-                         "tensor_tflops_at_algorithmic_flops": tflops,
-                         "kernel_ms_per_launch": kernel_ms,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+                       "l2": f"rotating {nsets} input/output sets = {nsets * per_set / 2**20:.0f} MiB > 126 MiB L2",
+                       "launch": "python loop" if a.no_graph else "CUDA graph replay (one fused kernel per step)"},
+            "roofline": roof,
             "latency_ms": {"p50": nearest_rank(per_step_ms, 50), "p99": nearest_rank(per_step_ms, 99),
                            "batch": rows, "kind": "device (CUDA events), per batch"},
             "cpu_baseline": cpu,
@@ -360,7 +415,10 @@ def latency_sweep(model, local, f):
         torch.cuda.synchronize()
         dev_ms = []
         for _ in range(300):
+            # a queued spin keeps the GPU busy while the host enqueues the events
+            # and the launch, so e0 -> e1 is device time only (no host overhead)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(100_000)
             e0.record(stream)
             runner.run(x)
             e1.record(stream)

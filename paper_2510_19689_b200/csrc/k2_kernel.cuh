@@ -234,10 +234,11 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   const uint32_t bar_id = 1 + g;
   uint32_t dphase = 0, xphase = 0;
 
-  // stage this warp's rows [r0w, r0w + nw) of x into xst (TMA bulk + tail)
-  auto load_x = [&](int64_t r0w, int nw) {
-    const int ne = nw * F;
-    const int nb = x_bulk_ok ? ((ne * 4) & ~15) / 4 : 0;
+  // stage this warp's rows [r0w, r0w + nw) of x into xst: the TMA bulk part is
+  // issued early (issue_x), the unaligned tail is loaded by the lanes (wait_x)
+  auto x_bulk_elems = [&](int nw) -> int { return x_bulk_ok ? ((nw * F * 4) & ~15) / 4 : 0; };
+  auto issue_x = [&](int64_t r0w, int nw) {
+    const int nb = x_bulk_elems(nw);
     if (lane == 0) {
       if (nb > 0) {
         ptx::mbar_arrive_expect_tx(&bars->xfull[warp], (uint32_t)nb * 4u);
@@ -246,10 +247,20 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         ptx::mbar_arrive(&bars->xfull[warp]);
       }
     }
+  };
+  auto wait_x = [&](int64_t r0w, int nw) {
+    const int ne = nw * F, nb = x_bulk_elems(nw);
     for (int e = nb + lane; e < 32 * F; e += 32) xst[e] = e < ne ? __ldg(a.x + r0w * F + e) : 0.0f;
     ptx::mbar_wait(&bars->xfull[warp], xphase);
     xphase ^= 1;
     __syncwarp();
+  };
+  // rows of this warp in the tile of group-local index m (0 when past the end)
+  auto warp_rows = [&](int64_t m, int64_t& r0w) -> int {
+    const int64_t r0 = ((int64_t)blockIdx.x + (int64_t)gridDim.x * m) * 128;
+    r0w = r0 + q * 32;
+    const int64_t n = a.rows - r0w;
+    return m >= tiles_cta || n <= 0 ? 0 : (n > 32 ? 32 : (int)n);
   };
   // stg (32 x F, this warp's rows) -> dst rows [0, nw): bulk store when aligned
   auto flush = [&](float* dst, int nw) {
@@ -277,6 +288,11 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     if (old == (v / NSLOT) * NG + NG - 1 && v + NSLOT < nblk) ring_load(v + NSLOT);
   };
 
+  {   // this warp's first x tile streams in with the weights
+    int64_t r0w;
+    const int nw0 = warp_rows(g, r0w);
+    if (nw0 > 0) issue_x(r0w, nw0);
+  }
   ptx::mbar_wait(&bars->cfull, 0);
   if (a.scale) {     // batch-statistics control: override the affine in this CTA's copy
     float* cw = reinterpret_cast<float*>(smem);
@@ -392,10 +408,21 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
 
     // ---- x -> xn (network.py:118-120), prior = 1, agg = 0 ----
     if (tr) TBN_TRACE(g * 4000 + 3000 + 8 * (int)k);
-    claim_stg();
-    ptx::fence_async_shared();
-    __syncwarp();
-    if (nw > 0) load_x(r0w, nw);
+    if (k > 0) {                  // (round 0's x was issued in the prologue)
+      claim_stg();
+      ptx::fence_async_shared();
+      __syncwarp();
+      if (nw > 0) issue_x(r0w, nw);
+    }
+    if (nw > 0) wait_x(r0w, nw);
+    {   // warm L2 with this warp's rows of the group's next tile
+      int64_t r0n;
+      const int nwn = warp_rows(m + NG, r0n);
+      if (lane == 0 && nwn > 0 && x_bulk_ok) {
+        const uint32_t bytes = (uint32_t)((nwn * F * 4) & ~15);
+        if (bytes) ptx::bulk_prefetch_l2(a.x + r0n * F, bytes);
+      }
+    }
     if (tr) TBN_TRACE(g * 4000 + 3001 + 8 * (int)k);
     {
       int bad = 0;

@@ -100,8 +100,11 @@ struct Cfg {
   static constexpr bool S_OK = NG_S > NG_R && (S_RES || S_SLOTS >= 3);
   static constexpr bool XS = S_OK;                     // xn in shared memory
   static constexpr int NG = XS ? NG_S : NG_R;
-  static constexpr bool RING = XS && !S_RES;
-  static constexpr int NSLOT = RING ? S_SLOTS : 0;
+  // fc1/fc2 blocks resident, or streamed through the ring when the image does not fit
+  static constexpr int STG_ALL = (XS ? 2 : 1) * (NG * 4) * STG;
+  static constexpr bool RING = IMG_BYTES + STG_ALL > SMEM_MAX;
+  static constexpr int NSLOT = RING ? cmin(6, (SMEM_MAX - FIX_S - STG_ALL) / HBR) : 0;
+  static_assert(!RING || NSLOT >= 2, "not even a 2-slot weight ring fits");
   static constexpr int NB = 2 * (S + 1);               // ring blocks per tile: fc1_s, fc2_s
   static_assert(NG >= 1, "per-row state does not fit");
   static constexpr int TCOLS = pow2ceil(NG * TCG);

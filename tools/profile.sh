@@ -7,5 +7,5 @@ CFG=${1:-hr}; PREC=${2:-tf32x3}; TAG=${3:-r1}
 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
     --log-file gpurun_out/launches_${CFG}_${PREC}_${TAG}.csv \
     python bench.py --config $CFG --precision $PREC --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null
-ncu --set full --import-source on --clock-control none -k regex:tabnet_fused -s 3 -c 1 \
+ncu --set full --import-source on --clock-control none -k regex:"tabnet_(fused|rowthread)" -s 3 -c 1 \
     -o gpurun_out/full_${CFG}_${PREC}_${TAG} python tools/prof_run.py --config $CFG --precision $PREC > /dev/null

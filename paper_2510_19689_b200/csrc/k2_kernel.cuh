@@ -177,7 +177,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   constexpr int NB = CF::NB, NSLOT = CF::NSLOT;
   const float* cst = reinterpret_cast<const float*>(smem);
   Bars* bars = reinterpret_cast<Bars*>(smem + CF::OFF_BAR);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so the TMEM and SMEM
+  // addresses derived from it live in uniform registers (no R2UR per tcgen05 op)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int g = warp >> 2, q = warp & 3;
   const int t = q * 32 + lane;                      // row within the tile == TMEM lane
   const int64_t ntiles = (a.rows + 127) / 128;
@@ -234,7 +236,10 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   float* stg = reinterpret_cast<float*>(smem + CF::OFF_STG + warp * CF::STG);
   // where x lands and xn lives: its own per-warp tile (variant S) or the staging tile
   float* xst = CF::XS ? reinterpret_cast<float*>(smem + CF::OFF_XS + warp * CF::STG) : stg;
-  const uint32_t bar_id = 1 + g;
+  float* const my_stg = stg + lane * F;             // this thread's row in the staging tile
+  float* const my_xs = xst + lane * F;
+  const uint32_t bar_id = 1 + g;                    // A ready (before the MMA issue)
+  const uint32_t bar_done = 1 + NG + g;             // D ready (after warp 0 saw the commit)
   uint32_t dphase = 0, xphase = 0;
 
   // stage this warp's rows [r0w, r0w + nw) of x into xst: the TMA bulk part is
@@ -334,8 +339,11 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     }
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 2);
     post();
-    ptx::mbar_wait(&bars->dfull[g], dphase);
+    // warp 0 polls the commit barrier; the other three sleep in bar.sync instead
+    // of spinning on the mbarrier (a spin costs issue slots the other groups use)
+    if (q == 0) ptx::mbar_wait(&bars->dfull[g], dphase);
     dphase ^= 1;
+    ptx::named_bar_sync(bar_done, 128);
     ptx::tc_fence_after();
     if constexpr (CF::RING) {
       if (rv >= 0 && tr) ring_release((uint32_t)rv);
@@ -347,7 +355,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
 
   float xnr[CF::XS ? 1 : F], agg[F], gv[H], lacc[C];
   auto xn_at = [&](int f) -> float {
-    if constexpr (CF::XS) return xst[lane * F + f];
+    if constexpr (CF::XS) return my_xs[f];
     else return xnr[f];
   };
 
@@ -432,7 +440,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       float xv[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) {
-        xv[f] = nw > 0 ? xst[lane * F + f] : 0.0f;
+        xv[f] = nw > 0 ? my_xs[f] : 0.0f;
         bad |= !isfinite(xv[f]);
         agg[f] = 0.0f;
       }
@@ -450,7 +458,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
 #pragma unroll
       for (int f = 0; f < F; ++f) {
-        if constexpr (CF::XS) xst[lane * F + f] = xv[f];
+        if constexpr (CF::XS) my_xs[f] = xv[f];
         else xnr[f] = xv[f];
       }
       float one[F];
@@ -518,7 +526,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         for (int f = 0; f < F; ++f) agg[f] = 0.0f;
       }
 #pragma unroll
-      for (int f = 0; f < F; ++f) agg[f] = fmaf(w, stg[lane * F + f], agg[f]);
+      for (int f = 0; f < F; ++f) agg[f] = fmaf(w, my_stg[f], agg[f]);
     };
 
     transform(0, nopost);                                        // network.py:226-227
@@ -630,8 +638,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
               const float2 xm = __fmul2_rn(mk, f2(xn_at(f), xn_at(f + 1)));    // network.py:238
               pr[i] = np.x; pr[i + 1] = np.y;
               av[i] = xm.x; av[i + 1] = xm.y;
-              stg[lane * F + f] = mk.x;
-              stg[lane * F + f + 1] = mk.y;
+              my_stg[f] = mk.x;
+              my_stg[f + 1] = mk.y;
             } else {
 #pragma unroll
               for (int u = 0; u < 2; ++u) {
@@ -640,7 +648,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
                   const float mk = fmaxf(z[fu] - tau, 0.0f);
                   pr[i + u] = pr[i + u] * (p.gamma - mk);
                   av[i + u] = mk * xn_at(fu);
-                  stg[lane * F + fu] = mk;
+                  my_stg[fu] = mk;
                 } else {
                   av[i + u] = fu == F ? 1.0f : 0.0f;                      // ones column (bias row)
                 }
@@ -690,7 +698,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       const float rdiv = __frcp_rn(div);
       claim_stg();
 #pragma unroll
-      for (int f = 0; f < F; ++f) stg[lane * F + f] = agg[f] * rdiv;
+      for (int f = 0; f < F; ++f) my_stg[f] = agg[f] * rdiv;
       if (a.importance && nw > 0) flush(a.importance + r0w * F, nw);
     }
     if (tr) TBN_TRACE(g * 4000 + 3003 + 8 * (int)k);

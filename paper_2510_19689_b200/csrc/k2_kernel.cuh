@@ -103,7 +103,8 @@ struct Cfg {
   // fc1/fc2 blocks resident, or streamed through the ring when the image does not fit
   static constexpr int STG_ALL = (XS ? 2 : 1) * (NG * 4) * STG;
   static constexpr bool RING = IMG_BYTES + STG_ALL > SMEM_MAX;
-  static constexpr int NSLOT = RING ? cmin(6, (SMEM_MAX - FIX_S - STG_ALL) / HBR) : 0;
+  static constexpr int NSLOT_FIT = RING ? cmin(8, (SMEM_MAX - FIX_S - STG_ALL) / HBR) : 0;
+  static constexpr int NSLOT = NSLOT_FIT >= 8 ? 8 : NSLOT_FIT >= 4 ? 4 : NSLOT_FIT >= 2 ? 2 : 0;  // power of 2
   static_assert(!RING || NSLOT >= 2, "not even a 2-slot weight ring fits");
   static constexpr int NB = 2 * (S + 1);               // ring blocks per tile: fc1_s, fc2_s
   static_assert(NG >= 1, "per-row state does not fit");
@@ -316,6 +317,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   // block rv).  The group meets at its barrier, warp 0 of the group issues the
   // chain and commits it; `post` overlaps the MMA; then everyone waits for D.
   int jt = 0;                                    // trace: GEMM counter
+  int64_t ring_pending = -1;                     // ring block awaiting release (tr thread)
   const bool tr = (q == 0 && lane == 0);
   auto gemm = [&](int kind, uint32_t bo, int64_t rv, auto&& post) {
     if (tr) TBN_TRACE(g * 4000 + 4 * jt);
@@ -336,6 +338,14 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tA, wbase + bo);
       else tc::issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tA, wbase + bo);
       ptx::mma_commit(&bars->dfull[g]);
+      if constexpr (CF::RING) {
+        // the previous GEMM's ring block: its MMAs completed before this chain
+        // was issued, so release it now, off the critical path
+        if (lane == 0 && ring_pending >= 0) {
+          ring_release((uint32_t)ring_pending);
+          ring_pending = -1;
+        }
+      }
     }
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 2);
     post();
@@ -346,7 +356,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     ptx::named_bar_sync(bar_done, 128);
     ptx::tc_fence_after();
     if constexpr (CF::RING) {
-      if (rv >= 0 && tr) ring_release((uint32_t)rv);
+      if (rv >= 0 && tr) ring_pending = rv;      // released under the next MMA chain
     }
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 3);
     ++jt;
@@ -399,6 +409,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       // no tile for this group in the last round: release its ring blocks
       if constexpr (CF::RING) {
         if (tr) {
+          if (ring_pending >= 0) ring_release((uint32_t)ring_pending);
+          ring_pending = -1;
           for (uint32_t i = 0; i < (uint32_t)NB; ++i) {
             const uint32_t v = (uint32_t)(k * NB) + i;
             ptx::mbar_wait(&bars->rfull[v % NSLOT], (v / NSLOT) & 1u);
@@ -702,6 +714,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       if (a.importance && nw > 0) flush(a.importance + r0w * F, nw);
     }
     if (tr) TBN_TRACE(g * 4000 + 3003 + 8 * (int)k);
+  }
+  if constexpr (CF::RING) {
+    if (tr && ring_pending >= 0) ring_release((uint32_t)ring_pending);
   }
   if (lane == 0) ptx::bulk_wait0();
 

@@ -186,7 +186,9 @@ def run_reference(a) -> None:
         "value": value, "unit": "rows/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.description, "rows_per_step": rows, "regime": a.regime},
+        "config": {"workload": w.description, "rows_per_step": rows, "regime": a.regime,
+                   "head": "regression (logit column 0 of the 2-class reference)" if w.regression
+                   else "softmax classifier"},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": "port",
                          "sample": f"{rows} rows/step of {a.config} ({a.regime} weights), "
                                    f"oracle/tabnet_oracle.py over {procs} fork-pool processes"},
@@ -258,8 +260,7 @@ def run_ours(a) -> None:
     w = W.WORKLOADS[a.config]
     rows = a.rows or w.batch
     counts = W.algorithmic_counts(w)
-    model = TabNetModel.from_reference(W.make_model(a.config, a.regime), precision=a.precision,
-                                       device=local)
+    model = W.make_engine_model(a.config, a.regime, precision=a.precision, device=local)
     runner = DeviceRunner(model, rows, device=local)
     f = w.feature_count
     # rotating input/output sets so the timed region always streams from HBM
@@ -405,7 +406,10 @@ def run_ours(a) -> None:
                                            "bf16": "bf16", "fp32": "fp32 (CUDA-core FFMA)"}[a.precision],
             "data": "synthetic",
             "config": {"workload": w.description, "rows_per_rank": rows, "regime": a.regime,
-                       "precision": a.precision, "outputs": "logits, probabilities, masks (S,B,F), importance, class",
+                       "head": "regression (TabNetRegressor, identity head)" if w.regression
+                       else "softmax classifier",
+                       "precision": a.precision, "outputs": ("output value, masks (S,B,F), importance" if w.regression else
+                                   "logits, probabilities, masks (S,B,F), importance, class"),
                        "parallelism": f"row-shard x{world} (no collective)",
                        "l2": f"rotating {nsets} input/output sets = {nsets * per_set / 2**20:.0f} MiB > 126 MiB L2",
                        "launch": "python loop" if a.no_graph else

@@ -46,6 +46,14 @@ typedef enum {
   TBN_PREC_FP32 = 3    /* CUDA-core fp32 FFMA kernel (no tensor cores; reference-precision check)     */
 } tbn_precision;
 
+/* tbn_config.flags.  TBN_CFG_REGRESSION: identity head, n_classes must be 1.
+ * An extension: the reference only has the
+ * softmax classifier (config.py:32-33 enforces n_classes >= 2).  The output
+ * is logits (rows, 1) = d_sum @ head_W + head_b; probabilities (if requested)
+ * receive the same value and predicted_class is 0.  Its oracle is column 0 of
+ * the reference logits of a 2-class model sharing head_W[:, 0] / head_b[0]. */
+#define TBN_CFG_REGRESSION 1
+
 /* apply() flags (network.py:195-196) */
 #define TBN_FLAG_NORMALIZED 1u      /* input is already normalized: skip the frozen affine        */
 #define TBN_FLAG_BATCH_STATS 2u     /* negative control: normalize with this batch's mean/var     */
@@ -56,7 +64,7 @@ typedef struct {
   int32_t n_d;           /* decision width               */
   int32_t n_a;           /* attention width              */
   int32_t n_steps;       /* S                            */
-  int32_t reserved;
+  int32_t flags;         /* TBN_CFG_* (0 = the reference's classifier)          */
   double gamma;          /* prior relaxation (config.py:26) */
 } tbn_config;
 

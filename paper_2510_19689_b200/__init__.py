@@ -10,14 +10,14 @@ from .errors import (ChecksumError, ConfigurationError, DeviceError, FormatVersi
                      InvalidInputError, ModelFormatError, TabserveError, TruncatedStreamError,
                      UnsupportedShapeError)
 from .network import (DEFAULT_PRECISION, Explanation, ForwardResult, GpuTabNetModel,
-                      PredictionOutput, TabNetModel, init_parameters)
+                      PredictionOutput, TabNetModel, TabNetRegressor, init_parameters)
 from .sparsemax import project_simplex_bruteforce, sparsemax
 from .io import load_model, load_model_file, save_model, save_model_file
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ModelConfig", "TabNetModel", "GpuTabNetModel", "Explanation", "PredictionOutput",
+    "ModelConfig", "TabNetModel", "GpuTabNetModel", "TabNetRegressor", "Explanation", "PredictionOutput",
     "ForwardResult", "init_parameters", "sparsemax", "project_simplex_bruteforce",
     "save_model", "load_model", "save_model_file", "load_model_file", "DEFAULT_PRECISION",
     "TabserveError", "InvalidInputError", "ConfigurationError", "ModelFormatError",

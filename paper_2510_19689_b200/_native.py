@@ -19,6 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libtabnet_b200.so"
 
 TBN_OK, TBN_ERR_INVALID_INPUT, TBN_ERR_CONFIG, TBN_ERR_CUDA, TBN_ERR_UNSUPPORTED = range(5)
 PREC_TF32X3, PREC_TF32, PREC_BF16, PREC_FP32 = range(4)
+CFG_REGRESSION = 1           # tbn_config.flags: identity head, n_classes == 1
 PRECISIONS = {"tf32x3": PREC_TF32X3, "tf32": PREC_TF32, "bf16": PREC_BF16, "fp32": PREC_FP32}
 FLAG_NORMALIZED = 1
 FLAG_BATCH_STATS = 2
@@ -34,7 +35,7 @@ EXPORTED = (
 
 class TbnConfig(C.Structure):
     _fields_ = [("feature_count", C.c_int32), ("n_classes", C.c_int32), ("n_d", C.c_int32),
-                ("n_a", C.c_int32), ("n_steps", C.c_int32), ("reserved", C.c_int32),
+                ("n_a", C.c_int32), ("n_steps", C.c_int32), ("flags", C.c_int32),
                 ("gamma", C.c_double)]
 
 

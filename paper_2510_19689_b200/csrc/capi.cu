@@ -55,6 +55,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct tbn_model {
   tbn_config cfg{};
+  bool regression = false;     // TBN_CFG_REGRESSION: identity head, logits only
   int precision = TBN_PREC_TF32X3;
   int device = 0;
   int num_sms = 148;
@@ -88,7 +89,11 @@ tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,
   const tbn_config c = *cfg;
   // ModelConfig.__post_init__ (config.py:29-41)
   if (c.feature_count < 1) return fail(TBN_ERR_CONFIG, "feature_count must be >= 1");
-  if (c.n_classes < 2) return fail(TBN_ERR_CONFIG, "n_classes must be >= 2");
+  const bool regression = (c.flags & TBN_CFG_REGRESSION) != 0;
+  if (c.flags & ~TBN_CFG_REGRESSION) return fail(TBN_ERR_CONFIG, "unknown config flags");
+  if (regression ? c.n_classes != 1 : c.n_classes < 2)
+    return fail(TBN_ERR_CONFIG, regression ? "a regression head has n_classes == 1"
+                                           : "n_classes must be >= 2");
   if (c.n_d < 1 || c.n_a < 1) return fail(TBN_ERR_CONFIG, "n_d and n_a must be >= 1");
   if (c.n_steps < 1) return fail(TBN_ERR_CONFIG, "n_steps must be >= 1");
   if (!(c.gamma >= 1.0)) return fail(TBN_ERR_CONFIG, "gamma must be >= 1");
@@ -150,6 +155,7 @@ tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,
   tbn_model* m = new tbn_model();
   m->cfg = c;
   m->precision = precision;
+  m->regression = regression;
   m->device = device;
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
 
@@ -261,6 +267,11 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
   if (out) {
     a.logits = out->logits; a.probs = out->probabilities; a.masks = out->masks;
     a.importance = out->importance; a.pred = out->predicted_class;
+    if (m->regression) {        // identity head: the kernels write the logits only
+      if (!a.logits) a.logits = a.probs;
+      a.probs = nullptr;
+      a.pred = nullptr;
+    }
   }
   a.err_flag = err_flag;
   if (flags & TBN_FLAG_BATCH_STATS) {
@@ -403,6 +414,12 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   const size_t F = m->cfg.feature_count, C = m->cfg.n_classes, S = m->cfg.n_steps;
   OutT o{};
   if (out) o = *out;
+  const OutT user = o;
+  if (m->regression) {          // identity head: compute the logits only, fill the rest below
+    if (!o.logits) o.logits = o.probabilities;
+    o.probabilities = nullptr;
+    o.predicted_class = nullptr;
+  }
   constexpr bool kF32 = sizeof(T) == 4;
   const bool direct = kF32 && is_pinned(x) && is_pinned(o.logits) && is_pinned(o.probabilities) &&
                       is_pinned(o.masks) && is_pinned(o.importance) && is_pinned(o.predicted_class);
@@ -490,6 +507,11 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     if (st != TBN_OK) return st;
   }
   if (err_any) return fail(TBN_ERR_INVALID_INPUT, "features must be finite");
+  if (m->regression) {
+    if (user.probabilities && user.probabilities != o.logits)
+      std::memcpy(user.probabilities, o.logits, (size_t)rows * sizeof(*o.logits));
+    if (user.predicted_class) std::memset(user.predicted_class, 0, (size_t)rows * 4);
+  }
   return TBN_OK;
 }
 

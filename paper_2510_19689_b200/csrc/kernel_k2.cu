@@ -91,6 +91,7 @@ const K2Instance kK2[] = {
     TBN_K2(35, 16, 16, 5, 2, tc::kPrecTF32),   // HR
     TBN_K2(35, 16, 16, 5, 2, tc::kPrecBF16),
     TBN_K2(64, 32, 32, 5, 2, tc::kPrecBF16),   // BLS (its 2-class reference model)
+    TBN_K2(64, 32, 32, 5, 1, tc::kPrecBF16),   // BLS regression head (TBN_CFG_REGRESSION)
 };
 
 const K2Instance* find_k2(const HostParams& hp, int precision) {

@@ -125,6 +125,8 @@ const Instance kInstances[] = {
     TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecTF32x3), // BLS
     TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecTF32),
     TBN_INSTANCE(64, 32, 32, 5, 2, tc::kPrecBF16),
+    TBN_INSTANCE(64, 32, 32, 5, 1, tc::kPrecTF32x3), // BLS regression head (TBN_CFG_REGRESSION)
+    TBN_INSTANCE(64, 32, 32, 5, 1, tc::kPrecTF32),
 };
 
 const Instance* find(const HostParams& hp, int precision) {

@@ -21,6 +21,10 @@ class DeviceRunner:
         self.model = model
         dev = torch.cuda.current_device() if device is None else device
         self.engine = model.engine(device=dev)
+        self.n_out = self.engine.n_out
+        if self.n_out == 1 and getattr(model, "n_outputs", None) == 1:
+            # regression head: the kernel writes the one output value only
+            outputs = tuple(k for k in outputs if k not in ("probabilities", "predicted_class"))
         self.device = torch.device("cuda", dev)
         self.max_rows = max_rows
         self.flags = flags
@@ -32,7 +36,7 @@ class DeviceRunner:
 
     def alloc_outputs(self, rows: int) -> dict:
         cfg = self.model.config
-        f, c, s = cfg.feature_count, cfg.n_classes, cfg.n_steps
+        f, c, s = cfg.feature_count, self.n_out, cfg.n_steps
         shapes = dict(logits=(rows, c), probabilities=(rows, c), masks=(s, rows, f),
                       importance=(rows, f), predicted_class=(rows,))
         return {k: torch.empty(shapes[k], dtype=torch.int32 if k == "predicted_class" else torch.float32,
@@ -42,7 +46,7 @@ class DeviceRunner:
         """Outputs for a ``rows``-row call carved from the preallocated buffers
         (masks keep the step-major (S, rows, F) layout of network.py:231)."""
         cfg = self.model.config
-        f, c, s = cfg.feature_count, cfg.n_classes, cfg.n_steps
+        f, c, s = cfg.feature_count, self.n_out, cfg.n_steps
         shapes = dict(logits=(rows, c), probabilities=(rows, c), masks=(s, rows, f),
                       importance=(rows, f), predicted_class=(rows,))
         out = {}

@@ -93,12 +93,13 @@ class DeviceModel:
     """Owner of one ``tbn_model*`` (packed weights resident on one GPU)."""
 
     def __init__(self, config: ModelConfig, params: dict, norm_mean: np.ndarray,
-                 norm_var: np.ndarray, precision: str, device: int):
+                 norm_var: np.ndarray, precision: str, device: int, *, regression: bool = False):
         L = N.lib()
         if precision not in N.PRECISIONS:
             raise ConfigurationError(f"unknown precision {precision!r}; one of {sorted(N.PRECISIONS)}")
-        cfg = N.TbnConfig(config.feature_count, config.n_classes, config.n_d, config.n_a,
-                          config.n_steps, 0, float(config.gamma))
+        self.n_out = 1 if regression else config.n_classes
+        cfg = N.TbnConfig(config.feature_count, self.n_out, config.n_d, config.n_a,
+                          config.n_steps, N.CFG_REGRESSION if regression else 0, float(config.gamma))
         keys = sorted(params)
         arrays = [np.ascontiguousarray(params[k], dtype=np.float64) for k in keys]
         names = (C.c_char_p * len(keys))(*[k.encode() for k in keys])
@@ -131,7 +132,7 @@ class DeviceModel:
     # -- host-buffer path (reference-facing) ----------------------------------
     def forward_host_f64(self, x: np.ndarray, flags: int, want_masks: bool = True) -> dict:
         cfg = self.config
-        b, f, c, s = x.shape[0], cfg.feature_count, cfg.n_classes, cfg.n_steps
+        b, f, c, s = x.shape[0], cfg.feature_count, self.n_out, cfg.n_steps
         out = dict(logits=np.empty((b, c)), probabilities=np.empty((b, c)),
                    masks=np.empty((s, b, f)) if want_masks else None,
                    importance=np.empty((b, f)),
@@ -210,16 +211,17 @@ class TabNetModel:
                     if prec == "auto":
                         for cand in AUTO_ORDER:
                             try:
-                                eng = DeviceModel(self.config, self.params, self.norm_mean,
-                                                  self.norm_var, cand, dev)
+                                eng = self._make_engine(cand, dev)
                                 break
                             except UnsupportedShapeError:
                                 continue
                     else:
-                        eng = DeviceModel(self.config, self.params, self.norm_mean, self.norm_var,
-                                          prec, dev)
+                        eng = self._make_engine(prec, dev)
                     self._engines[key] = eng
         return eng
+
+    def _make_engine(self, precision: str, device: int) -> DeviceModel:
+        return DeviceModel(self.config, self.params, self.norm_mean, self.norm_var, precision, device)
 
     # -- normalization (network.py:118-120; host helper, not the hot path) -------
     def normalize(self, x: np.ndarray) -> np.ndarray:
@@ -267,8 +269,9 @@ class TabNetModel:
                 f"batch width {x.shape[-1] if x.ndim else 0} != feature_count {cfg.feature_count}")
         b = x.shape[0]
         if b == 0:
-            return ForwardResult(logits=np.empty((0, cfg.n_classes)),
-                                 probabilities=np.empty((0, cfg.n_classes)),
+            n_out = getattr(self, "n_outputs", cfg.n_classes)
+            return ForwardResult(logits=np.empty((0, n_out)),
+                                 probabilities=np.empty((0, n_out)),
                                  masks=np.empty((cfg.n_steps, 0, cfg.feature_count)),
                                  importance=np.empty((0, cfg.feature_count)))
         flags = (N.FLAG_NORMALIZED if normalized else 0) | \
@@ -300,3 +303,54 @@ class TabNetModel:
 
 
 GpuTabNetModel = TabNetModel
+
+
+@dataclass
+class TabNetRegressor(TabNetModel):
+    """Regression head on the same encoder (an extension).
+
+    The reference supports only the softmax classifier (config.py:32-33 enforces
+    ``n_classes >= 2``).  BASELINE's BLS workload is a regression, so the engine
+    offers an identity head: ``logits = d_sum @ head_W[:, c] + head_b[c]`` for one
+    column ``c`` of a reference model's head (``TBN_CFG_REGRESSION`` in the C ABI).
+    ``apply`` returns logits of shape (B, 1) and the same values as
+    ``probabilities``; masks and importance are the classifier's.  Its oracle is
+    column ``c`` of the reference's logits (network.py:253).
+    """
+
+    head_column: int = 0
+    n_outputs: int = 1
+
+    @classmethod
+    def from_reference(cls, model, *, head_column: int = 0, precision: str = DEFAULT_PRECISION,
+                       device: int | None = None) -> "TabNetRegressor":
+        base = TabNetModel.from_reference(model, precision=precision, device=device)
+        if not 0 <= head_column < base.config.n_classes:
+            raise ConfigurationError(f"head_column {head_column} outside the head's "
+                                     f"{base.config.n_classes} columns")
+        return cls(config=base.config, params=base.params, norm_mean=base.norm_mean,
+                   norm_var=base.norm_var, model_version=base.model_version,
+                   precision=precision, device=device, head_column=head_column)
+
+    def _make_engine(self, precision: str, device: int) -> DeviceModel:
+        c = self.head_column
+        params = dict(self.params)
+        params["head_W"] = np.ascontiguousarray(np.asarray(self.params["head_W"])[:, c:c + 1])
+        params["head_b"] = np.ascontiguousarray(np.asarray(self.params["head_b"])[c:c + 1])
+        return DeviceModel(self.config, params, self.norm_mean, self.norm_var, precision, device,
+                           regression=True)
+
+    def forward(self, batch) -> list[PredictionOutput]:
+        values = getattr(batch, "values", batch)
+        result = self.apply(values)
+        return [PredictionOutput(probabilities=result.logits[i], predicted_class=0,
+                                 explanation=Explanation(step_masks=result.masks[:, i, :].copy(),
+                                                         aggregate_importance=result.importance[i].copy()))
+                for i in range(result.logits.shape[0])]
+
+    def copy(self) -> "TabNetRegressor":
+        return TabNetRegressor(config=self.config,
+                               params={k: v.copy() for k, v in self.params.items()},
+                               norm_mean=self.norm_mean.copy(), norm_var=self.norm_var.copy(),
+                               model_version=self.model_version, precision=self.precision,
+                               device=self.device, head_column=self.head_column)

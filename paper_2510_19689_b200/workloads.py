@@ -25,6 +25,7 @@ class Workload:
     n_classes: int
     batch: int
     description: str
+    regression: bool = False     # evaluated through TabNetRegressor (identity head on column 0)
 
     def model_config(self, seed: int = 0) -> ModelConfig:
         return ModelConfig(feature_count=self.feature_count, n_classes=self.n_classes,
@@ -32,16 +33,17 @@ class Workload:
 
 
 # BASELINE.json "configs" in order.  BLS is a regression in BASELINE.json; the
-# reference has no regression head (config.py:32-33), so the engine evaluates it
-# as the 2-class model whose logit column 0 is the regression output
-# (SURVEY.md §0.6 / §8(a) A11).
+# reference has no regression head (config.py:32-33), so the workload's weights
+# are the 2-class reference model and the engine runs TabNetRegressor, the
+# identity head on its logit column 0.
 WORKLOADS: dict[str, Workload] = {
     "adult": Workload("adult", 0, 14, 8, 8, 3, 2, 4096,
                       "Adult-shaped (14 features, n_d=n_a=8, n_steps=3, binary) batch 4,096"),
     "hr": Workload("hr", 1, 35, 16, 16, 5, 2, 65536,
                    "HR-attrition-shaped (35 features, n_d=n_a=16, n_steps=5) batch 65,536, with feature masks"),
     "bls": Workload("bls", 2, 64, 32, 32, 5, 2, 262144,
-                    "BLS-shaped (64 features, n_d=n_a=32, n_steps=5) batch 262,144, row-sharded"),
+                    "BLS-shaped synthetic regression (64 features, n_d=n_a=32, n_steps=5) batch "
+                    "262,144, row-sharded", regression=True),
     "hr_latency": Workload("hr_latency", 3, 35, 16, 16, 5, 2, 1024,
                            "HR shape latency sweep batch 1-1,024"),
     "wide": Workload("wide", 4, 512, 64, 64, 8, 10, 1 << 24,
@@ -80,6 +82,15 @@ def make_inputs(w: Workload, rows: int, seed: int | None = None, start: int = 0)
     return rng.standard_normal((rows, w.feature_count), dtype=np.float32)
 
 
+def make_engine_model(name: str, regime: str = "trained", *, precision: str = "auto",
+                      device: int | None = None):
+    """The engine model a workload runs: TabNetModel, or TabNetRegressor for the
+    regression workload (BLS)."""
+    from .network import TabNetModel, TabNetRegressor
+    cls = TabNetRegressor if WORKLOADS[name].regression else TabNetModel
+    return cls.from_reference(make_model(name, regime), precision=precision, device=device)
+
+
 def make_model(name: str, regime: str = "trained", *, model_cls=None):
     """A TabNetModel (this package's, or ``model_cls``) for a named workload."""
     from .network import TabNetModel
@@ -91,10 +102,13 @@ def make_model(name: str, regime: str = "trained", *, model_cls=None):
 
 
 def algorithmic_counts(w: Workload) -> dict:
-    """Per-row algorithmic FLOPs and HBM bytes."""
-    f, nd, na, s, c = w.feature_count, w.n_d, w.n_a, w.n_steps, w.n_classes
+    """Per-row algorithmic FLOPs and HBM bytes.
+    A regression head (C=1) writes its one output value and no class."""
+    f, nd, na, s = w.feature_count, w.n_d, w.n_a, w.n_steps
     h = nd + na
+    c = 1 if w.regression else w.n_classes
+    out_b = 4 if w.regression else 8 * c + 4              # logits (+ probs + class)
     flops = 2 * ((s + 1) * (2 * h * f + 6 * h * h) + s * na * f + nd * c)
-    bytes_pe = 4 * f + 4 * s * f + 4 * f + 8 * c + 4     # x, masks, importance, logits+probs, class
-    bytes_po = 4 * f + 8 * c + 4                          # predict-only
+    bytes_pe = 4 * f + 4 * s * f + 4 * f + out_b          # x, masks, importance, head outputs
+    bytes_po = 4 * f + out_b                              # predict-only
     return dict(flops_per_row=flops, bytes_per_row=bytes_pe, bytes_per_row_predict=bytes_po)

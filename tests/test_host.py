@@ -115,6 +115,52 @@ def test_algorithmic_counts_match_survey():
     assert W.algorithmic_counts(W.WORKLOADS["wide"])["flops_per_row"] == 4654336
     assert W.algorithmic_counts(W.WORKLOADS["adult"])["bytes_per_row"] == 300
     assert W.algorithmic_counts(W.WORKLOADS["hr"])["bytes_per_row"] == 1000
+    # BLS is the regression workload (C=1, one output value, no class)
+    assert W.algorithmic_counts(W.WORKLOADS["bls"])["flops_per_row"] == 413760
+    assert W.algorithmic_counts(W.WORKLOADS["bls"])["bytes_per_row"] == 1796
+
+
+def _create(cfg_flags, n_classes, params_cfg):
+    L = N.lib()
+    cfg = N.TbnConfig(params_cfg.feature_count, n_classes, params_cfg.n_d, params_cfg.n_a,
+                      params_cfg.n_steps, cfg_flags, 1.3)
+    p = P.init_parameters(params_cfg)
+    if n_classes == 1:
+        p["head_W"] = p["head_W"][:, :1].copy()
+        p["head_b"] = p["head_b"][:1].copy()
+    keys = sorted(p)
+    arrs = [np.ascontiguousarray(p[k]) for k in keys]
+    names = (ctypes.c_char_p * len(keys))(*[k.encode() for k in keys])
+    vals = (ctypes.c_void_p * len(keys))(*[a.ctypes.data for a in arrs])
+    sizes = (ctypes.c_int64 * len(keys))(*[a.size for a in arrs])
+    mean, var = np.zeros(params_cfg.feature_count), np.ones(params_cfg.feature_count)
+    h = ctypes.c_void_p()
+    st = L.tbn_model_create(ctypes.byref(cfg), names, vals, sizes, len(keys), mean.ctypes.data,
+                            var.ctypes.data, 0, 0, ctypes.byref(h))
+    if h.value:
+        L.tbn_model_destroy(h)
+    return st, L.tbn_last_error().decode()
+
+
+def test_regression_config_validation_in_the_c_abi():
+    """TBN_CFG_REGRESSION (the identity-head extension) needs n_classes == 1;
+    without it the reference's n_classes >= 2 rule holds (config.py:32-33)."""
+    cfg = P.ModelConfig(feature_count=5, n_d=4, n_a=4, n_steps=2)
+    st, msg = _create(N.CFG_REGRESSION, 2, cfg)
+    assert st == 2 and "n_classes == 1" in msg
+    st, msg = _create(0, 1, cfg)
+    assert st == 2 and "n_classes must be >= 2" in msg
+    st, msg = _create(4, 2, cfg)
+    assert st == 2 and "flags" in msg
+    st, _ = _create(N.CFG_REGRESSION, 1, cfg)
+    assert st in (0, 3, 4)          # valid config: OK on a GPU box, CUDA/UNSUPPORTED without one
+
+
+def test_regressor_head_column_validation():
+    with pytest.raises(P.ConfigurationError):
+        P.TabNetRegressor.from_reference(W.make_model("bls"), head_column=2)
+    r = P.TabNetRegressor.from_reference(W.make_model("bls"), head_column=1)
+    assert r.head_column == 1 and r.n_outputs == 1
 
 
 def test_workload_inputs_are_a_stream():

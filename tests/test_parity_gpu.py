@@ -251,3 +251,33 @@ def test_bf16_stated_bound(case):
     print(case, "bf16", rep.summary())
     assert not rep.class_mismatch_rows, rep.summary()
     assert rep.max_err["probabilities"] < 3e-2 and rep.viol["masks"] == 0 and rep.viol["importance"] == 0
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("regime", ["init", "trained"])
+def test_regression_head_against_reference_logit_column(precision, regime):
+    """TabNetRegressor (identity head, TBN_CFG_REGRESSION): its output is column 0
+    of the reference's logits (network.py:253) of the 2-class BLS model; masks
+    and importance are the classifier's.  Exact modes under the tie-aware rule,
+    single-pass modes under their stated bounds."""
+    g = load_golden(f"bls_{regime}")
+    base = golden_model(f"bls_{regime}", precision)
+    m = P.TabNetRegressor.from_reference(base, head_column=0, precision=precision)
+    r = m.apply(g["x"].astype(np.float64))
+    assert r.logits.shape == (g["x"].shape[0], 1) and np.array_equal(r.probabilities, r.logits)
+    ref = dict(g)
+    ref["logits"] = g["logits"][:, :1]
+    got = dict(logits=r.logits, probabilities=g["probabilities"], masks=r.masks,
+               importance=r.importance)
+    if precision in EXACT_PRECISIONS:
+        rep = compare(ref, got)
+        assert rep.ok, rep.summary()
+    else:
+        rtol = 5e-2 if precision == "tf32" else 1.5e-1
+        rep = compare(ref, got, delta=0.0, gap=1.0, rtol=rtol,
+                      atol={"logits": 5e-2 if precision == "tf32" else 2e-1})
+        assert rep.viol["masks"] == 0 and rep.viol["importance"] == 0 and rep.viol["logits"] == 0, \
+            rep.summary()
+    # predict-only device path: no probabilities/class buffers are needed
+    eng = m.engine()
+    assert eng.n_out == 1

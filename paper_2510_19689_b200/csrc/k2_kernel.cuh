@@ -240,7 +240,6 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   float* const my_stg = stg + lane * F;             // this thread's row in the staging tile
   float* const my_xs = xst + lane * F;
   const uint32_t bar_id = 1 + g;                    // A ready (before the MMA issue)
-  const uint32_t bar_done = 1 + NG + g;             // D ready (after warp 0 saw the commit)
   uint32_t dphase = 0, xphase = 0;
 
   // stage this warp's rows [r0w, r0w + nw) of x into xst: the TMA bulk part is
@@ -351,9 +350,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     post();
     // warp 0 polls the commit barrier; the other three sleep in bar.sync instead
     // of spinning on the mbarrier (a spin costs issue slots the other groups use)
-    if (q == 0) ptx::mbar_wait(&bars->dfull[g], dphase);
+    // every warp parks on the commit barrier (suspend-time hint: no spinning)
+    ptx::mbar_wait_sleep(&bars->dfull[g], dphase);
     dphase ^= 1;
-    ptx::named_bar_sync(bar_done, 128);
     ptx::tc_fence_after();
     if constexpr (CF::RING) {
       if (rv >= 0 && tr) ring_pending = rv;      // released under the next MMA chain
@@ -371,7 +370,11 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
 
   // GLU block over D = [lin' | gate'] (H + H columns): gv <- lin'(1+t) [+ R gv]
   auto glu = [&](bool residual) {
+#ifdef TBN_K2_CW16
+    constexpr int CW = H < 16 ? H : 16;
+#else
     constexpr int CW = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);
+#endif
     static_assert(H % CW == 0, "GLU chunking");
     float lin[CW], gate[CW];
     tmem_load_n<CW>(tD, lin);
@@ -602,6 +605,22 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         tau = fmaxf(-1.0f, bound - 9.5367431640625e-07f * fmaxf(1.0f, fabsf(bound)));
         float cnt_prev = (float)(F + 1);
         for (int it = 0; it <= F; ++it) {
+#ifdef TBN_K2_ACC4
+          float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
+          float2 sc = f2(0.0f, 0.0f), cc = f2(0.0f, 0.0f), sd = f2(0.0f, 0.0f), cd = f2(0.0f, 0.0f);
+#pragma unroll
+          for (int i = 0; i + 1 < F; i += 2) {
+            const float2 mk = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
+            switch ((i / 2) % 4) {
+              case 0: sa = __ffma2_rn(mk, f2(z[i], z[i + 1]), sa); ca = __fadd2_rn(ca, mk); break;
+              case 1: sb = __ffma2_rn(mk, f2(z[i], z[i + 1]), sb); cb = __fadd2_rn(cb, mk); break;
+              case 2: sc = __ffma2_rn(mk, f2(z[i], z[i + 1]), sc); cc = __fadd2_rn(cc, mk); break;
+              default: sd = __ffma2_rn(mk, f2(z[i], z[i + 1]), sd); cd = __fadd2_rn(cd, mk); break;
+            }
+          }
+          const float2 s2 = __fadd2_rn(__fadd2_rn(sa, sb), __fadd2_rn(sc, sd));
+          const float2 c2 = __fadd2_rn(__fadd2_rn(ca, cb), __fadd2_rn(cc, cd));
+#else
           float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
 #pragma unroll
           for (int i = 0; i + 1 < F; i += 2) {
@@ -615,6 +634,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
             }
           }
           const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
+#endif
           float sm = s2.x + s2.y, cn = c2.x + c2.y;
           if constexpr (F % 2) {
             const float mk = z[F - 1] > tau ? 1.0f : 0.0f;

@@ -48,6 +48,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Blocking wait with a suspend-time hint: the warp is parked by the hardware
+// until the phase completes (or the hint elapses) instead of spinning.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "TBN_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra.uni TBN_WAITS_%=;\n\t}"
+      ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
 // ---- async proxy fences ---------------------------------------------------
 // Generic-proxy shared-memory writes (st.shared) -> visible to the tensor core.
 __device__ __forceinline__ void fence_async_shared() {

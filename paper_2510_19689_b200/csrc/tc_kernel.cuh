@@ -379,7 +379,13 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
   constexpr int HH = CF::HH, KH = CF::KH, K1 = CF::K1;
   const float* cst = reinterpret_cast<const float*>(smem + SM::OFF_CONST);
   Bars* bars = reinterpret_cast<Bars*>(smem + SM::OFF_BAR);
+#ifdef TBN_K1_PLAINWARP
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#else
+  // warp index through a shuffle: provably warp-uniform, so TMEM/SMEM addresses
+  // derived from it live in uniform registers (no R2UR per tcgen05 op)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+#endif
   const int64_t ntiles = (a.rows + 127) / 128;
   const int64_t npairs = (ntiles + NG - 1) / NG;
   const bool x_bulk_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0);

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <unistd.h>
 #include <map>
 #include <mutex>
 #include <string>
@@ -242,9 +243,13 @@ tbn_status tbn_model_info(const tbn_model* m, tbn_config* cfg, int32_t* precisio
 }
 
 size_t tbn_workspace_bytes(const tbn_model* m, int64_t rows, uint32_t flags) {
-  (void)rows;
   size_t b = 256;
   if (m && (flags & TBN_FLAG_BATCH_STATS)) b += align_up(2 * (size_t)m->cfg.feature_count * sizeof(float), 256);
+  if (m && m->tc.scratch_per_cta) {      // K3 row-tile state: one slice per CTA of the grid
+    const int64_t tiles = (rows + 127) / 128;
+    const int64_t grid = tiles < m->num_sms ? tiles : m->num_sms;
+    b += (size_t)(grid > 0 ? grid : 1) * m->tc.scratch_per_cta;
+  }
   return b;
 }
 
@@ -274,6 +279,10 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
     }
   }
   a.err_flag = err_flag;
+  if (m->tc.scratch_per_cta)             // K3 scratch after the batch-stats block
+    a.scratch = (float*)((char*)workspace + 256 +
+                         ((flags & TBN_FLAG_BATCH_STATS)
+                              ? align_up(2 * (size_t)m->cfg.feature_count * sizeof(float), 256) : 0));
   if (flags & TBN_FLAG_BATCH_STATS) {
     float* ss = (float*)((char*)workspace + 256);
     a.scale = ss;
@@ -283,8 +292,19 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
   // Development aid: TBN_TRACE=1 records a clock64 timeline of CTA 0 and
   // prints it to stderr after a synchronizing copy (never set in production).
   static const bool trace_on = getenv("TBN_TRACE") != nullptr;
+  // TBN_TRACE_MAPPED: the timeline lives in mapped host memory and the host
+  // polls it while the kernel runs, so a hung kernel still shows how far it got
+  static const bool trace_mapped = getenv("TBN_TRACE_MAPPED") != nullptr;
   static unsigned long long* d_trace = nullptr;
-  if (trace_on && m->precision != TBN_PREC_FP32) {
+  static unsigned long long* h_trace = nullptr;
+  if (trace_mapped && m->precision != TBN_PREC_FP32) {
+    if (!h_trace) {
+      cudaHostAlloc((void**)&h_trace, 16384 * sizeof(unsigned long long), cudaHostAllocMapped);
+      cudaHostGetDevicePointer((void**)&d_trace, h_trace, 0);
+    }
+    std::memset(h_trace, 0, 16384 * sizeof(unsigned long long));
+    a.trace = d_trace;
+  } else if (trace_on && m->precision != TBN_PREC_FP32) {
     if (!d_trace) cudaMalloc(&d_trace, 16384 * sizeof(unsigned long long));
     cudaMemsetAsync(d_trace, 0, 16384 * sizeof(unsigned long long), s);
     a.trace = d_trace;
@@ -295,7 +315,14 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
   else
     e = tbn::launch_tc(m->tc, a, m->num_sms, s);
   if (e != cudaSuccess) return cuda_fail(e, "forward kernel launch");
-  if (a.trace) {
+  if (a.trace && trace_mapped) {
+    for (int i = 0; i < 200 && cudaStreamQuery(s) == cudaErrorNotReady; ++i) usleep(50000);
+    const bool hung = cudaStreamQuery(s) == cudaErrorNotReady;
+    fprintf(stderr, "TRACE rows=%lld %s\n", (long long)rows, hung ? "HUNG" : "done");
+    for (int k = 0; k < 16384; ++k)
+      if (((volatile unsigned long long*)h_trace)[k]) fprintf(stderr, "TRACE %d %llu\n", k, ((volatile unsigned long long*)h_trace)[k]);
+    if (hung) _exit(3);
+  } else if (a.trace) {
     std::vector<unsigned long long> h(16384);
     cudaMemcpyAsync(h.data(), d_trace, 16384 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);

@@ -1,0 +1,140 @@
+// kernel_k3.cu — host side of K3 (k3_kernel.cuh), the wide-model kernel: its
+// weight packer and instance.  Every B operand is cut into K-chunks of at most
+// 32 KB, each a standalone N x Kc K-major canonical block (bf16, round to
+// nearest even from the float64 weight), stored back to back in the order the
+// kernel streams them.  GLU constants are folded as in K2 (tanh form).
+#include <cmath>
+#include <cstring>
+#include <vector>
+#include "tbn_tc.h"
+#include "k3_kernel.cuh"
+#include "pack_util.h"
+
+namespace tbn {
+
+namespace {
+
+// W (Kin x N row-major, x @ W) -> chunks of kc rows of K (last may be short),
+// element (n, k) of a chunk at (n/8)*(kc*8) + (k/8)*64 + (n%8)*8 + k%8.
+// Row k == Kin carries the bias (when given); rows beyond are zero.
+void pack_chunked(std::vector<uint16_t>& img, size_t off_bytes, const double* W, int Kin, int N,
+                  int Ktot, int kc_max, const std::vector<double>* colscale, const double* bias) {
+  size_t base = off_bytes / 2;
+  for (int k0 = 0; k0 < Ktot; k0 += kc_max) {
+    const int kc = Ktot - k0 < kc_max ? Ktot - k0 : kc_max;
+    for (int n = 0; n < N; ++n)
+      for (int kl = 0; kl < kc; ++kl) {
+        const int k = k0 + kl;
+        double w = k < Kin ? W[(size_t)k * N + n] : (bias && k == Kin ? bias[n] : 0.0);
+        if (colscale) w *= (*colscale)[n];
+        img[base + (size_t)(n / 8) * (kc * 8) + (kl / 8) * 64 + (n % 8) * 8 + (kl % 8)] =
+            pack::bf16_rn_host((float)w);
+      }
+    base += (size_t)N * kc;
+  }
+}
+
+template <class CF>
+bool pack_k3(const HostParams& hp, TcModel* out, std::string* err) {
+  constexpr int F = CF::F, H = CF::H, N2 = CF::N2, S = CF::S, ND = CF::ND, NA = CF::NA, C = CF::C;
+  std::vector<uint16_t> img(CF::IMG_BYTES / 2, 0);
+  float* cst = reinterpret_cast<float*>(img.data());
+  const double kR = 0.70710678118654752440;
+  for (int f = 0; f < F; ++f) {
+    cst[CF::C_SCALE + f] = (float)(1.0 / std::sqrt(hp.norm_var[f] + 1e-8));   // network.py:120
+    cst[CF::C_SHIFT + f] = (float)hp.norm_mean[f];
+  }
+  for (int n = 0; n < N2; ++n) cst[CF::C_B1 + n] = (float)(hp.sh1_b[n] * 0.5);  // shared1 bias, tanh-folded
+  for (int i = 0; i < ND * C; ++i) cst[CF::C_HW + i] = (float)hp.head_W[i];
+  for (int i = 0; i < C; ++i) cst[CF::C_HB + i] = (float)hp.head_b[i];
+  std::vector<double> cs_first(N2, 0.5), cs_res(N2);
+  for (int n = 0; n < N2; ++n) cs_res[n] = n < H ? 0.5 * kR : 0.5;
+  pack_chunked(img, CF::O_SH1, hp.sh1_W, F, N2, CF::K1, CF::KC_N2, &cs_first, nullptr);
+  pack_chunked(img, CF::O_SH2, hp.sh2_W, H, N2, CF::KHID, CF::KC_N2, &cs_res, hp.sh2_b);
+  for (int s = 0; s <= S; ++s) {
+    pack_chunked(img, CF::O_FC1 + (size_t)s * CF::BLK_HID, hp.fc1_W[s], H, N2, CF::KHID, CF::KC_N2,
+                 &cs_res, hp.fc1_b[s]);
+    pack_chunked(img, CF::O_FC2 + (size_t)s * CF::BLK_HID, hp.fc2_W[s], H, N2, CF::KHID, CF::KC_N2,
+                 &cs_res, hp.fc2_b[s]);
+  }
+  for (int s = 1; s <= S; ++s)
+    pack_chunked(img, CF::O_ATT + (size_t)(s - 1) * CF::BLK_ATT, hp.att_W[s], NA, F, CF::KATT,
+                 CF::KC_ATT, nullptr, hp.att_b[s]);
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, CF::IMG_BYTES);
+  if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), CF::IMG_BYTES, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (d) cudaFree(d);
+    if (err) *err = cudaGetErrorString(e);
+    return false;
+  }
+  out->d_buf = d;
+  out->bytes = CF::IMG_BYTES;
+  out->scratch_per_cta = CF::SCRATCH_PER_CTA;
+  out->params = new k3::Params{(const uint8_t*)d, (float)hp.gamma};
+  return true;
+}
+
+template <class CF>
+cudaError_t launch_k3_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k3::tabnet_wide<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         CF::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (!a.scratch) return cudaErrorInvalidValue;
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  k3::tabnet_wide<CF><<<grid, CF::THREADS, CF::SMEM_BYTES, stream>>>(*(const k3::Params*)m.params, a);
+  return cudaGetLastError();
+}
+
+struct K3Instance {
+  int F, ND, NA, S, C;
+  bool (*pack)(const HostParams&, TcModel*, std::string*);
+  cudaError_t (*launch)(const TcModel&, const ForwardArgs&, int, cudaStream_t);
+};
+
+#define TBN_K3(F, ND, NA, S, C) \
+  K3Instance{F, ND, NA, S, C, &pack_k3<k3::Cfg<F, ND, NA, S, C>>, &launch_k3_impl<k3::Cfg<F, ND, NA, S, C>>}
+
+const K3Instance kK3[] = {
+    TBN_K3(512, 64, 64, 8, 10),   // wide (BASELINE config 5)
+};
+
+const K3Instance* find_k3(const HostParams& hp, int precision) {
+  if (precision != 2) return nullptr;          // bf16 only
+  for (const K3Instance& in : kK3)
+    if (in.F == hp.F && in.ND == hp.ND && in.NA == hp.NA && in.S == hp.S && in.C == hp.C) return &in;
+  return nullptr;
+}
+
+}  // namespace
+
+bool k3_supported(const HostParams& hp, int precision) { return find_k3(hp, precision) != nullptr; }
+
+bool k3_pack(const HostParams& hp, int precision, TcModel* out, std::string* err) {
+  const K3Instance* in = find_k3(hp, precision);
+  if (!in) {
+    if (err) *err = "no K3 instance";
+    return false;
+  }
+  out->shape_id = (int)(in - kK3);
+  return in->pack(hp, out, err);
+}
+
+void k3_free(TcModel* m) {
+  if (m->d_buf) cudaFree(m->d_buf);
+  delete (k3::Params*)m->params;
+  m->d_buf = nullptr;
+  m->params = nullptr;
+}
+
+cudaError_t k3_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  if (m.shape_id < 0) return cudaErrorInvalidValue;
+  return kK3[m.shape_id].launch(m, a, num_sms, stream);
+}
+
+}  // namespace tbn

@@ -142,7 +142,7 @@ const Instance* find(const HostParams& hp, int precision) {
 }  // namespace
 
 bool tc_supported(const HostParams& hp, int precision) {
-  return k2_supported(hp, precision) || find(hp, precision) != nullptr;
+  return k3_supported(hp, precision) || k2_supported(hp, precision) || find(hp, precision) != nullptr;
 }
 
 // K2 (k2_kernel.cuh) serves the single-pass modes wherever an instance exists;
@@ -153,6 +153,11 @@ static bool k2_allowed() {
 }
 
 bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err) {
+  if (k3_supported(hp, precision)) {
+    out->kernel = 3;
+    out->precision = precision;
+    return k3_pack(hp, precision, out, err);
+  }
   if (k2_allowed() && k2_supported(hp, precision)) {
     out->kernel = 2;
     out->precision = precision;
@@ -170,6 +175,10 @@ bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err
 }
 
 void tc_free(TcModel* m) {
+  if (m->kernel == 3) {
+    k3_free(m);
+    return;
+  }
   if (m->kernel == 2) {
     k2_free(m);
     return;
@@ -181,6 +190,7 @@ void tc_free(TcModel* m) {
 }
 
 cudaError_t launch_tc(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  if (m.kernel == 3) return k3_launch(m, a, num_sms, stream);
   if (m.kernel == 2) return k2_launch(m, a, num_sms, stream);
   if (m.shape_id < 0) return cudaErrorInvalidValue;
   return kInstances[m.shape_id].launch(m, a, num_sms, stream);

@@ -32,6 +32,7 @@ struct ForwardArgs {
   float* importance;
   int32_t* pred;
   int32_t* err_flag;
+  float* scratch;              // K3: per-CTA row-tile state in the workspace
   unsigned long long* trace;   // debug timeline (TBN_TRACE env); null in production
 };
 

@@ -22,11 +22,12 @@ struct HostParams {
 };
 
 struct TcModel {
-  int kernel = 1;          // 1: K1 (tc_kernel.cuh), 2: K2 (k2_kernel.cuh)
+  int kernel = 1;          // 1: K1 (tc_kernel.cuh), 2: K2 (k2_kernel.cuh), 3: K3 (k3_kernel.cuh)
   int shape_id = -1;       // which compiled instance
   int precision = 0;
   void* d_buf = nullptr;   // packed operands + epilogue constants
   size_t bytes = 0;
+  size_t scratch_per_cta = 0;   // K3: global per-CTA row-tile state (prior, agg, mask)
   void* params = nullptr;  // host copy of the kernel's parameter block
 };
 
@@ -40,5 +41,11 @@ bool k2_supported(const HostParams& hp, int precision);
 bool k2_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
 void k2_free(TcModel* m);
 cudaError_t k2_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream);
+
+// K3, the wide-model design (kernel_k3.cu)
+bool k3_supported(const HostParams& hp, int precision);
+bool k3_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
+void k3_free(TcModel* m);
+cudaError_t k3_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream);
 
 }  // namespace tbn

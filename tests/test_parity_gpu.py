@@ -238,7 +238,7 @@ def test_auto_precision_selects_a_gpu_kernel():
     assert rep.ok, rep.summary()
 
 
-@pytest.mark.parametrize("case", [f"{n}_{r}" for n in TC_SHAPES for r in ("init", "trained")])
+@pytest.mark.parametrize("case", [f"{n}_{r}" for n in TC_SHAPES + ("wide",) for r in ("init", "trained")])
 def test_bf16_stated_bound(case):
     """BF16 operands (kind::f16, fp32 accumulate): the stated looser bound
     (8-bit mantissa operands; SURVEY.md §8(c) emulation, re-measured on B200):
@@ -281,3 +281,15 @@ def test_regression_head_against_reference_logit_column(precision, regime):
     # predict-only device path: no probabilities/class buffers are needed
     eng = m.engine()
     assert eng.n_out == 1
+
+
+def test_wide_bf16_kernel_batch_invariance():
+    """K3 (wide, F=512): per-row results are bitwise independent of the batch and
+    of the row's position in its 128-row tile (network.py:11-14)."""
+    m = golden_model("wide_trained", "bf16")
+    x = W.make_inputs(W.WORKLOADS["wide"], 300).astype(np.float64)
+    full = m.apply(x)
+    parts = [m.apply(x[a:b]) for a, b in ((0, 1), (1, 130), (130, 300))]
+    assert np.array_equal(np.concatenate([p.probabilities for p in parts]), full.probabilities)
+    assert np.array_equal(np.concatenate([p.masks for p in parts], axis=1), full.masks)
+    assert np.array_equal(np.concatenate([p.importance for p in parts]), full.importance)

@@ -253,7 +253,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
   // the ring -> everyone waits for D.  a_smem: A from SMEM (attentive) or TMEM.
   // kind: 0 = N2 output with A from TMEM, 1 = attentive (N = F, A in SMEM).
   uint32_t gcount = 0;
-  auto gemm = [&](int kind, int nch, uint32_t tA, uint32_t tD) {
+  auto gemm = [&](int kind, int nch, uint32_t tA, uint32_t tD, auto&& post) {
     if (lane == 0 && warp < 2) TBN_K3T(100 + warp * 400 + (gcount % 200) * 2, clock64());
     ptx::tmem_st_wait();
     ptx::fence_async_shared();
@@ -309,6 +309,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       }
       ptx::mma_commit(&bars->dfull);
     }
+    post();                                          // CUDA-core work in the MMA's shadow
     if (lane == 0 && warp < 2) TBN_K3T(101 + warp * 400 + (gcount % 200) * 2, clock64());
     ptx::mbar_wait_sleep(&bars->dfull, dphase);
     dphase ^= 1;
@@ -379,17 +380,18 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       tmem_store_n<8>(tq + T_A + H / 2, ones);
     }
   };
+  auto nopost = [] {};
   auto transform = [&]() {
-    gemm(0, CF::NCH_SH1, tq + T_A, tq + T_D);
+    gemm(0, CF::NCH_SH1, tq + T_A, tq + T_D, nopost);
     glu(false, true);
     store_g();
-    gemm(0, CF::NCH_HID, tq + T_A, tq + T_D);
+    gemm(0, CF::NCH_HID, tq + T_A, tq + T_D, nopost);
     glu(true, false);
     store_g();
-    gemm(0, CF::NCH_HID, tq + T_A, tq + T_D);
+    gemm(0, CF::NCH_HID, tq + T_A, tq + T_D, nopost);
     glu(true, false);
     store_g();
-    gemm(0, CF::NCH_HID, tq + T_A, tq + T_D);
+    gemm(0, CF::NCH_HID, tq + T_A, tq + T_D, nopost);
     glu(true, false);
   };
   // A_att (SMEM, canonical K-major no-swizzle): element (row, k) at
@@ -460,23 +462,49 @@ tabnet_wide(const Params p, const ForwardArgs a) {
     transform();                                     // network.py:226-227
     store_att_a();                                   // A of step 1's attentive GEMM
 
+    // agg += eta_s * m_s (network.py:245) needs step s's eta, known after its
+    // transform; it runs in the shadow of step s+1's attentive MMA
+    bool agg_pend = false, agg_zero = false;
+    float agg_w = 0.0f;
+    const float* agg_m = nullptr;
+    bool agg_mw = false;
+    auto agg_update = [&]() {
+      if (!agg_pend) return;
+      agg_pend = false;
+#pragma unroll 1
+      for (int o = 0; o < FS; o += 32) {
+        float mv[32], ag[32];
+        if (agg_mw) ld32(agg_m + o, mv);
+        else
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mv[i] = 0.0f;
+        if (agg_zero) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ag[i] = 0.0f;
+        } else {
+          ld32(my_agg + o, ag);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ag[i] = fmaf(agg_w, mv[i], ag[i]);
+        st32(my_agg + o, ag);
+      }
+    };
+
     for (int s = 1; s <= S; ++s) {
       // ---- attentive transformer: z = prior * (a @ W_att + b) (network.py:233-235) ----
-      gemm(1, CF::NCH_ATT, 0, tq + T_ATT);
+      gemm(1, CF::NCH_ATT, 0, tq + T_ATT, agg_update);
       if (threadIdx.x == 0) TBN_K3T(1000 + 10 * s, clock64());
       // z' = prior * z in TMEM; slice max / sum
       float pmax = -INFINITY, psum = 0.0f;
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
-        float z[32];
+        float z[32], pr[32];
+        if (s > 1) ld32(my_prior + o, pr);           // in flight with the TMEM load
         tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
         ptx::tmem_ld_wait();
         if (s > 1) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 pv = *reinterpret_cast<const float4*>(my_prior + o + i);
-            z[i] *= pv.x; z[i + 1] *= pv.y; z[i + 2] *= pv.z; z[i + 3] *= pv.w;
-          }
+          for (int i = 0; i < 32; ++i) z[i] *= pr[i];
           tmem_store_n<32>(tq + T_ATT + c * FS + o, z);
         }
 #pragma unroll
@@ -585,24 +613,13 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       const bool reset = all_eta_zero && eta > 0.0f;
       const float w = all_eta_zero ? (eta > 0.0f ? eta : 1.0f) : eta;
       all_eta_zero = all_eta_zero && !(eta > 0.0f);
-#pragma unroll 1
-      for (int o = 0; o < FS; o += 32) {
-        float mv[32], ag[32];
-        if (mwrite) ld32(mrow + o, mv);
-        else
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mv[i] = 0.0f;
-        if (s == 1 || reset) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) ag[i] = 0.0f;
-        } else {
-          ld32(my_agg + o, ag);
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) ag[i] = fmaf(w, mv[i], ag[i]);
-        st32(my_agg + o, ag);
-      }
+      agg_pend = true;
+      agg_zero = (s == 1 || reset);
+      agg_w = w;
+      agg_m = mrow;
+      agg_mw = mwrite;
     }
+    agg_update();                                    // the last step's (no attentive MMA follows)
 
     // ---- head + softmax + argmax (network.py:253-256, :279) ----
     {

@@ -175,6 +175,21 @@ __device__ __forceinline__ void ld32(const float* p, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) { v[4 * i] = t[i].x; v[4 * i + 1] = t[i].y; v[4 * i + 2] = t[i].z; v[4 * i + 3] = t[i].w; }
 }
+// the same over a scratch in the coalesced [F/4][128 rows][4] layout: a row's
+// consecutive float4s are 128*4 floats apart, the 32 lanes (rows) of a warp hit
+// 512 consecutive bytes per access
+__device__ __forceinline__ void ld32s(const float* p, float (&v)[32]) {
+  float4 t[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t[i] = *reinterpret_cast<const float4*>(p + 512 * i);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { v[4 * i] = t[i].x; v[4 * i + 1] = t[i].y; v[4 * i + 2] = t[i].z; v[4 * i + 3] = t[i].w; }
+}
+__device__ __forceinline__ void st32s(float* p, const float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    *reinterpret_cast<float4*>(p + 512 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
 __device__ __forceinline__ void st32(float* p, const float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -203,9 +218,12 @@ tabnet_wide(const Params p, const ForwardArgs a) {
   float* prior_s = a.scratch + (size_t)blockIdx.x * (CF::SCRATCH_PER_CTA / 4);
   float* agg_s = prior_s + 128 * F;
   float* msk_s = agg_s + 128 * F;
-  float* my_prior = prior_s + (size_t)r * F + c * FS;
-  float* my_agg = agg_s + (size_t)r * F + c * FS;
-  float* my_msk = msk_s + (size_t)r * F + c * FS;
+  // scratch layout [F/4][128][4]: feature f of row r at ((f/4)*128 + r)*4 + f%4;
+  // my_*(o) = this thread's 32-feature run starting at slice feature o
+  const size_t sofs = (size_t)(c * FS / 4) * 512 + (size_t)r * 4;
+  float* my_prior = prior_s + sofs;
+  float* my_agg = agg_s + sofs;
+  float* my_msk = msk_s + sofs;
 
   const int64_t tiles_cta = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const uint32_t nchunks = (uint32_t)(tiles_cta * CF::TILE_CH);
@@ -466,27 +484,22 @@ tabnet_wide(const Params p, const ForwardArgs a) {
     // transform; it runs in the shadow of step s+1's attentive MMA
     bool agg_pend = false, agg_zero = false;
     float agg_w = 0.0f;
-    const float* agg_m = nullptr;
-    bool agg_mw = false;
     auto agg_update = [&]() {
       if (!agg_pend) return;
       agg_pend = false;
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float mv[32], ag[32];
-        if (agg_mw) ld32(agg_m + o, mv);
-        else
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mv[i] = 0.0f;
+        ld32s(my_msk + (o / 4) * 512, mv);
         if (agg_zero) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) ag[i] = 0.0f;
         } else {
-          ld32(my_agg + o, ag);
+          ld32s(my_agg + (o / 4) * 512, ag);
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) ag[i] = fmaf(agg_w, mv[i], ag[i]);
-        st32(my_agg + o, ag);
+        st32s(my_agg + (o / 4) * 512, ag);
       }
     };
 
@@ -499,7 +512,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
-        if (s > 1) ld32(my_prior + o, pr);           // in flight with the TMEM load
+        if (s > 1) ld32s(my_prior + (o / 4) * 512, pr);   // in flight with the TMEM load
         tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
         ptx::tmem_ld_wait();
         if (s > 1) {
@@ -556,12 +569,14 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       if (threadIdx.x == 0) TBN_K3T(1002 + 10 * s, clock64());
       // mask, prior update (network.py:236-237); the mask goes to the masks
       // output (or the scratch when none is requested), read back below
-      float* mrow = a.masks ? a.masks + ((int64_t)(s - 1) * a.rows + (valid ? row : 0)) * F + c * FS : my_msk;
-      const bool mwrite = a.masks ? valid : true;
+      // the mask goes to the coalesced scratch (read back for x*m and the agg
+      // update) and, when requested, to the masks output
+      float* mrow = a.masks ? a.masks + ((int64_t)(s - 1) * a.rows + (valid ? row : 0)) * F + c * FS : nullptr;
+      const bool mwrite = a.masks && valid;
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
-        if (s > 1) ld32(my_prior + o, pr);
+        if (s > 1) ld32s(my_prior + (o / 4) * 512, pr);
         tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
         ptx::tmem_ld_wait();
 #pragma unroll
@@ -570,7 +585,8 @@ tabnet_wide(const Params p, const ForwardArgs a) {
           pr[i] = (s > 1 ? pr[i] : 1.0f) * (p.gamma - mk);                   // network.py:237
           z[i] = mk;
         }
-        st32(my_prior + o, pr);
+        st32s(my_prior + (o / 4) * 512, pr);
+        st32s(my_msk + (o / 4) * 512, z);
         if (mwrite) st32(mrow + o, z);
       }
       if (threadIdx.x == 0) TBN_K3T(1003 + 10 * s, clock64());
@@ -579,10 +595,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float xv[32], mv[32];
-        if (mwrite) ld32(mrow + o, mv);
-        else
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mv[i] = 0.0f;
+        ld32s(my_msk + (o / 4) * 512, mv);
         xn_chunk(o, xv);
         float pk[16];
 #pragma unroll
@@ -616,8 +629,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       agg_pend = true;
       agg_zero = (s == 1 || reset);
       agg_w = w;
-      agg_m = mrow;
-      agg_mw = mwrite;
+
     }
     agg_update();                                    // the last step's (no attentive MMA follows)
 
@@ -654,7 +666,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float ag[32];
-        ld32(my_agg + o, ag);
+        ld32s(my_agg + (o / 4) * 512, ag);
 #pragma unroll
         for (int i = 0; i < 32; ++i) t0 += ag[i];
       }
@@ -667,7 +679,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
         for (int o = 0; o < FS; o += 32) {
           float ag[32];
-          ld32(my_agg + o, ag);
+          ld32s(my_agg + (o / 4) * 512, ag);
 #pragma unroll
           for (int i = 0; i < 32; ++i) ag[i] *= rdiv;
           st32(irow + o, ag);

@@ -14,7 +14,7 @@ ap.add_argument("--iters", type=int, default=5)
 a = ap.parse_args()
 w = W.WORKLOADS[a.config]
 rows = a.rows or w.batch
-m = TabNetModel.from_reference(W.make_model(a.config, "trained"), precision=a.precision, device=0)
+m = W.make_engine_model(a.config, "trained", precision=a.precision, device=0)
 r = DeviceRunner(m, rows, device=0)
 x = torch.from_numpy(W.make_inputs(w, rows)).cuda()
 for _ in range(a.iters):

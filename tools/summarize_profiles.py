@@ -26,7 +26,7 @@ hdr = next(i for i, l in enumerate(txt) if l.startswith('"ID"'))
 for r in csv.DictReader(io.StringIO("\n".join(txt[hdr:]))):
     rows.append((r["Kernel Name"], float(r["Metric Value"])))
 tot = sum(t for _, t in rows)
-fused = [t for n, t in rows if ("tabnet_fused" in n or "tabnet_rowthread" in n)]
+fused = [t for n, t in rows if ("tabnet_fused" in n or "tabnet_rowthread" in n or "tabnet_wide" in n)]
 share = sum(fused) / tot if tot else 0.0
 
 # ---- full capture ----

@@ -52,9 +52,9 @@ constexpr int pow2ceil(int v) { int p = 32; while (p < v) p <<= 1; return p; }
 template <int F_, int ND_, int NA_, int S_, int C_, int PREC_>
 struct Cfg {
   static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
-  static_assert(PREC == kPrecTF32 || PREC == kPrecBF16, "K2 covers the single-pass modes");
+  static_assert(PREC == kPrecTF32 || PREC == kPrecBF16 || PREC == tc::kPrecTF32x3, "K2 precision");
   static constexpr int H = ND + NA, N2 = 2 * H;
-  static constexpr bool X3 = false;
+  static constexpr bool X3 = (PREC == tc::kPrecTF32x3);   // 3xTF32: A and B split hi/lo, 3 MMAs
   static constexpr bool BF = (PREC == kPrecBF16);
   static constexpr int KG = BF ? 16 : 8;               // MMA K granule
   static constexpr int ESZ = BF ? 2 : 4;
@@ -66,7 +66,7 @@ struct Cfg {
   static constexpr int KA_EL = cmax(cmax(K1, KHID), KATT);
   static constexpr int KA = BF ? KA_EL / 2 : KA_EL;    // A operand TMEM columns
   static constexpr int DW = cmax(N2, FN);
-  static constexpr int T_D = 0, T_A = DW, T_PR = DW + KA, T_END = T_PR + F;
+  static constexpr int T_D = 0, T_A = DW, T_AL = T_A + KA, T_PR = T_AL + (X3 ? KA : 0), T_END = T_PR + F;
   static constexpr int TCG = rup(T_END, 32);           // TMEM columns per group
   static constexpr int NG_TMEM = 512 / TCG;
   // Register file: a row's live state is about 2F + H + 48 registers with xn
@@ -74,9 +74,10 @@ struct Cfg {
   static constexpr int NG_R = cmin(4, cmin(NG_TMEM, 65536 / (128 * (2 * F + H + 48))));
   static constexpr int NG_S = cmin(4, cmin(NG_TMEM, 65536 / (128 * (F + H + 48))));
   // weight blocks (B operands, N x K K-major canonical)
-  static constexpr int B_SH1 = N2 * K1 * ESZ;
-  static constexpr int B_HID = N2 * KHID * ESZ;
-  static constexpr int B_ATT = FN * KATT * ESZ;
+  static constexpr int PARTS = X3 ? 2 : 1;            // hi [+ lo] B blocks
+  static constexpr int B_SH1 = PARTS * N2 * K1 * ESZ;
+  static constexpr int B_HID = PARTS * N2 * KHID * ESZ;
+  static constexpr int B_ATT = PARTS * FN * KATT * ESZ;
   static constexpr int HBR = rup(B_HID, 128), ABR = rup(B_ATT, 128);
   // consts (floats): scale F | shift F | head_W ND*C | head_b C
   static constexpr int C_SCALE = 0, C_SHIFT = rup(F, 4), C_HW = C_SHIFT + rup(F, 4);
@@ -159,6 +160,14 @@ __device__ __forceinline__ void put_a(uint32_t tA, const float (&v)[M]) {
     tmem_store_n<L / 2>(tA + E / 2, pk);
   } else {
     tmem_store_n<L>(tA + E, v);
+    if constexpr (CF::X3) {
+      // 3xTF32: the MMA reads fp32 as tf32 by truncation, so A_hi = v and
+      // A_lo = v - trunc_tf32(v) (exact in fp32), stored KA columns further on
+      float lo[L];
+#pragma unroll
+      for (int i = 0; i < L; ++i) lo[i] = v[i] - __uint_as_float(__float_as_uint(v[i]) & 0xFFFFE000u);
+      tmem_store_n<L>(tA + CF::KA + E, lo);
+    }
   }
 }
 // A elements [E, E+L) = ones at element E, zeros after (the bias column)
@@ -333,9 +342,10 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
           bo = CF::OFF_RING + (v % NSLOT) * CF::HBR;
         }
       }
-      if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tA, wbase + bo);
-      else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tA, wbase + bo);
-      else tc::issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tA, wbase + bo);
+      const uint32_t tAL = tA + CF::KA;              // A_lo (3xTF32 only)
+      if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tAL, wbase + bo);
+      else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tAL, wbase + bo);
+      else tc::issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tAL, wbase + bo);
       ptx::mma_commit(&bars->dfull[g]);
       if constexpr (CF::RING) {
         // the previous GEMM's ring block: its MMAs completed before this chain
@@ -389,11 +399,24 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       }
 #pragma unroll
       for (int i = 0; i < CW; i += 2) {
-        const float2 th = f2(tanh_approx(gate[i]), tanh_approx(gate[i + 1]));
-        const float2 l = f2(lin[i], lin[i + 1]);
-        float2 w = l;
-        if (residual) w = __ffma2_rn(f2(gv[c0 + i], gv[c0 + i + 1]), f2(kR, kR), l);
-        const float2 o = __ffma2_rn(l, th, w);
+        float2 o;
+        if constexpr (CF::X3) {
+          // fp32-faithful sigmoid (as K1): gate columns carry -log2(e), so
+          // e = 2^gate' = exp(-u); one reciprocal per pair: q = 1/(d0 d1)
+          const float a0 = fminf(gate[i], 63.0f), a1 = fminf(gate[i + 1], 63.0f);
+          const float2 d = __fadd2_rn(f2(tc::ex2_approx(a0), tc::ex2_approx(a1)), f2(1.0f, 1.0f));
+          const float qq = tc::rcp_approx(d.x * d.y);
+          const float2 sg = __fmul2_rn(f2(d.y, d.x), f2(qq, qq));
+          const float2 l = f2(lin[i], lin[i + 1]);
+          o = residual ? __ffma2_rn(l, sg, __fmul2_rn(f2(gv[c0 + i], gv[c0 + i + 1]), f2(kR, kR)))
+                       : __fmul2_rn(l, sg);
+        } else {
+          const float2 th = f2(tanh_approx(gate[i]), tanh_approx(gate[i + 1]));
+          const float2 l = f2(lin[i], lin[i + 1]);
+          float2 w = l;
+          if (residual) w = __ffma2_rn(f2(gv[c0 + i], gv[c0 + i + 1]), f2(kR, kR), l);
+          o = __ffma2_rn(l, th, w);
+        }
         gv[c0 + i] = o.x;
         gv[c0 + i + 1] = o.y;
       }

@@ -33,25 +33,30 @@ bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
   }
   for (int i = 0; i < ND * C; ++i) img[CF::C_HW + i] = (float)hp.head_W[i];
   for (int i = 0; i < C; ++i) img[CF::C_HB + i] = (float)hp.head_b[i];
-  const double kR = 0.70710678118654752440;
+  const double kR = 0.70710678118654752440, kLog2e = 1.4426950408889634;
   std::vector<double> cs_first(N2), cs_res(N2);
   for (int n = 0; n < N2; ++n) {
-    cs_first[n] = 0.5;
-    cs_res[n] = n < H ? 0.5 * kR : 0.5;
+    if (CF::X3) {            // exact sigmoid: gate x -log2(e); residual linear x sqrt(.5)
+      cs_first[n] = n < H ? 1.0 : -kLog2e;
+      cs_res[n] = n < H ? kR : -kLog2e;
+    } else {                 // tanh form: everything x 1/2, residual linear x sqrt(.5)/2
+      cs_first[n] = 0.5;
+      cs_res[n] = n < H ? 0.5 * kR : 0.5;
+    }
   }
   using pack::pack_block;
   constexpr int HB = tc::rup(CF::B_HID, 128);
-  pack_block(img, CF::O_SH1 / 4, hp.sh1_W, F, N2, N2, CF::K1, false, N2, &cs_first, hp.sh1_b, CF::BF);
-  pack_block(img, CF::O_SH2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, false, N2, &cs_res, hp.sh2_b, CF::BF);
+  pack_block(img, CF::O_SH1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first, hp.sh1_b, CF::BF);
+  pack_block(img, CF::O_SH2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, CF::X3, N2, &cs_res, hp.sh2_b, CF::BF);
   for (int s = 0; s <= S; ++s) {
-    pack_block(img, (CF::O_FC1 + s * HB) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, false, N2, &cs_res,
+    pack_block(img, (CF::O_FC1 + s * HB) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
                hp.fc1_b[s], CF::BF);
-    pack_block(img, (CF::O_FC2 + s * HB) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, false, N2, &cs_res,
+    pack_block(img, (CF::O_FC2 + s * HB) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
                hp.fc2_b[s], CF::BF);
   }
   for (int s = 1; s <= S; ++s)
     pack_block(img, (CF::O_ATT + (s - 1) * tc::rup(CF::B_ATT, 128)) / 4, hp.att_W[s], NA, F, CF::FN, CF::KATT,
-               false, F, nullptr, hp.att_b[s], CF::BF);
+               CF::X3, F, nullptr, hp.att_b[s], CF::BF);
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, CF::IMG_BYTES);
   if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), CF::IMG_BYTES, cudaMemcpyHostToDevice);
@@ -86,6 +91,8 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
              &launch_k2_impl<k2::Cfg<F, ND, NA, S, C, P>>}
 
 const K2Instance kK2[] = {
+    TBN_K2(14, 8, 8, 3, 2, tc::kPrecTF32x3),   // Adult, 3xTF32 parity mode
+    TBN_K2(35, 16, 16, 5, 2, tc::kPrecTF32x3), // HR, 3xTF32 parity mode
     TBN_K2(14, 8, 8, 3, 2, tc::kPrecTF32),     // Adult
     TBN_K2(14, 8, 8, 3, 2, tc::kPrecBF16),
     TBN_K2(35, 16, 16, 5, 2, tc::kPrecTF32),   // HR
@@ -95,7 +102,8 @@ const K2Instance kK2[] = {
 };
 
 const K2Instance* find_k2(const HostParams& hp, int precision) {
-  const int prec = precision == 1 ? tc::kPrecTF32 : precision == 2 ? tc::kPrecBF16 : -1;
+  const int prec = precision == 0 ? tc::kPrecTF32x3 : precision == 1 ? tc::kPrecTF32
+                 : precision == 2 ? tc::kPrecBF16 : -1;
   for (const K2Instance& in : kK2)
     if (in.F == hp.F && in.ND == hp.ND && in.NA == hp.NA && in.S == hp.S && in.C == hp.C && in.prec == prec)
       return &in;

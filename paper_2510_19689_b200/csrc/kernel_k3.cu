@@ -4,6 +4,7 @@
 // nearest even from the float64 weight), stored back to back in the order the
 // kernel streams them.  GLU constants are folded as in K2 (tanh form).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "tbn_tc.h"
@@ -86,7 +87,9 @@ cudaError_t launch_k3_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   }
   if (!a.scratch) return cudaErrorInvalidValue;
   const int64_t ntiles = (a.rows + 127) / 128;
-  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  int cap = num_sms;
+  if (const char* e = std::getenv("TBN_K3_GRID")) cap = std::atoi(e) > 0 ? std::atoi(e) : num_sms;   // dev A/B
+  const int grid = (int)(ntiles < cap ? ntiles : cap);
   k3::tabnet_wide<CF><<<grid, CF::THREADS, CF::SMEM_BYTES, stream>>>(*(const k3::Params*)m.params, a);
   return cudaGetLastError();
 }

@@ -104,7 +104,8 @@ struct Cfg {
   // fc1/fc2 blocks resident, or streamed through the ring when the image does not fit
   static constexpr int STG_ALL = (XS ? 2 : 1) * (NG * 4) * STG;
   static constexpr bool RING = IMG_BYTES + STG_ALL > SMEM_MAX;
-  static constexpr int NSLOT_FIT = RING ? cmin(8, (SMEM_MAX - FIX_S - STG_ALL) / HBR) : 0;
+  // 4 slots (measured: 8 buys nothing and takes L1 away)
+  static constexpr int NSLOT_FIT = RING ? cmin(4, (SMEM_MAX - FIX_S - STG_ALL) / HBR) : 0;
   static constexpr int NSLOT = NSLOT_FIT >= 8 ? 8 : NSLOT_FIT >= 4 ? 4 : NSLOT_FIT >= 2 ? 2 : 0;  // power of 2
   static_assert(!RING || NSLOT >= 2, "not even a 2-slot weight ring fits");
   static constexpr int NB = 2 * (S + 1);               // ring blocks per tile: fc1_s, fc2_s
@@ -761,7 +762,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   if constexpr (CF::RING) {
     if (tr && ring_pending >= 0) ring_release((uint32_t)ring_pending);
   }
+#ifdef TBN_K2_ENDREAD
+  // the CTA's SMEM may be released once the bulk stores have READ it; their
+  // global writes complete with the grid
+  if (lane == 0) ptx::bulk_wait_read0();
+#else
   if (lane == 0) ptx::bulk_wait0();
+#endif
 
   ptx::tc_fence_before();
   __syncthreads();

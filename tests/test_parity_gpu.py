@@ -317,3 +317,25 @@ def test_wide_bf16_kernel_batch_invariance():
     assert np.array_equal(np.concatenate([p.probabilities for p in parts]), full.probabilities)
     assert np.array_equal(np.concatenate([p.masks for p in parts], axis=1), full.masks)
     assert np.array_equal(np.concatenate([p.importance for p in parts]), full.importance)
+
+
+@pytest.mark.parametrize("case,precision", [("hr_trained", "bf16"), ("hr_trained", "tf32x3"),
+                                            ("wide_trained", "bf16")])
+def test_normalized_flag_and_batch_stats(case, precision):
+    """apply(normalized=True) on host-normalized rows matches apply() (the frozen
+    affine, network.py:118-120, :212-220), and use_batch_stats normalizes with the
+    batch's own statistics (invariance.py:59's negative control) in every kernel."""
+    g = load_golden(case)
+    m = golden_model(case, precision)
+    x = g["x"].astype(np.float64)
+    r = m.apply(x)
+    xn = (x - g["norm_mean"]) / np.sqrt(g["norm_var"] + 1e-8)
+    rn = m.apply(xn.astype(np.float32).astype(np.float64), normalized=True)
+    tol = 2e-2 if precision == "bf16" else 1e-4
+    np.testing.assert_allclose(rn.probabilities, r.probabilities, atol=tol)
+    # batch statistics: same as normalizing with the batch mean/var by hand
+    mu, var = x.mean(axis=0), x.var(axis=0)
+    rb = m.apply(x, use_batch_stats=True)
+    rh = m.apply(((x - mu) / np.sqrt(var + 1e-8)).astype(np.float32).astype(np.float64), normalized=True)
+    np.testing.assert_allclose(rb.probabilities, rh.probabilities, atol=tol)
+    assert not np.allclose(rb.probabilities, r.probabilities, atol=1e-6)

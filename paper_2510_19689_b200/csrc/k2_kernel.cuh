@@ -381,11 +381,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
 
   // GLU block over D = [lin' | gate'] (H + H columns): gv <- lin'(1+t) [+ R gv]
   auto glu = [&](bool residual) {
-#ifdef TBN_K2_CW16
-    constexpr int CW = H < 16 ? H : 16;
-#else
-    constexpr int CW = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);
-#endif
+    constexpr int CW = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);   // 16 measured no faster
     static_assert(H % CW == 0, "GLU chunking");
     float lin[CW], gate[CW];
     tmem_load_n<CW>(tD, lin);
@@ -629,22 +625,6 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         tau = fmaxf(-1.0f, bound - 9.5367431640625e-07f * fmaxf(1.0f, fabsf(bound)));
         float cnt_prev = (float)(F + 1);
         for (int it = 0; it <= F; ++it) {
-#ifdef TBN_K2_ACC4
-          float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
-          float2 sc = f2(0.0f, 0.0f), cc = f2(0.0f, 0.0f), sd = f2(0.0f, 0.0f), cd = f2(0.0f, 0.0f);
-#pragma unroll
-          for (int i = 0; i + 1 < F; i += 2) {
-            const float2 mk = f2(z[i] > tau ? 1.0f : 0.0f, z[i + 1] > tau ? 1.0f : 0.0f);
-            switch ((i / 2) % 4) {
-              case 0: sa = __ffma2_rn(mk, f2(z[i], z[i + 1]), sa); ca = __fadd2_rn(ca, mk); break;
-              case 1: sb = __ffma2_rn(mk, f2(z[i], z[i + 1]), sb); cb = __fadd2_rn(cb, mk); break;
-              case 2: sc = __ffma2_rn(mk, f2(z[i], z[i + 1]), sc); cc = __fadd2_rn(cc, mk); break;
-              default: sd = __ffma2_rn(mk, f2(z[i], z[i + 1]), sd); cd = __fadd2_rn(cd, mk); break;
-            }
-          }
-          const float2 s2 = __fadd2_rn(__fadd2_rn(sa, sb), __fadd2_rn(sc, sd));
-          const float2 c2 = __fadd2_rn(__fadd2_rn(ca, cb), __fadd2_rn(cc, cd));
-#else
           float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f), sb = f2(0.0f, 0.0f), cb = f2(0.0f, 0.0f);
 #pragma unroll
           for (int i = 0; i + 1 < F; i += 2) {
@@ -658,7 +638,6 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
             }
           }
           const float2 s2 = __fadd2_rn(sa, sb), c2 = __fadd2_rn(ca, cb);
-#endif
           float sm = s2.x + s2.y, cn = c2.x + c2.y;
           if constexpr (F % 2) {
             const float mk = z[F - 1] > tau ? 1.0f : 0.0f;
@@ -762,13 +741,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   if constexpr (CF::RING) {
     if (tr && ring_pending >= 0) ring_release((uint32_t)ring_pending);
   }
-#ifdef TBN_K2_ENDREAD
-  // the CTA's SMEM may be released once the bulk stores have READ it; their
-  // global writes complete with the grid
-  if (lane == 0) ptx::bulk_wait_read0();
-#else
   if (lane == 0) ptx::bulk_wait0();
-#endif
 
   ptx::tc_fence_before();
   __syncthreads();

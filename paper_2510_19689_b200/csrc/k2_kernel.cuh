@@ -330,19 +330,21 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   const bool tr = (q == 0 && lane == 0);
   auto gemm = [&](int kind, uint32_t bo, int64_t rv, auto&& post) {
     if (tr) TBN_TRACE(g * 4000 + 4 * jt);
+    if constexpr (CF::RING) {
+      // the issuing warp checks its ring block while the other warps finish
+      // writing A (off the barrier -> MMA critical path)
+      if (rv >= 0) {
+        const uint32_t v = (uint32_t)rv;
+        if (q == 0) ptx::mbar_wait(&bars->rfull[v % NSLOT], (v / NSLOT) & 1u);
+        bo = CF::OFF_RING + (v % NSLOT) * CF::HBR;
+      }
+    }
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
     ptx::named_bar_sync(bar_id, 128);
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 1);
     if (q == 0) {
       ptx::tc_fence_after();
-      if constexpr (CF::RING) {
-        if (rv >= 0) {
-          const uint32_t v = (uint32_t)rv;
-          ptx::mbar_wait(&bars->rfull[v % NSLOT], (v / NSLOT) & 1u);
-          bo = CF::OFF_RING + (v % NSLOT) * CF::HBR;
-        }
-      }
       const uint32_t tAL = tA + CF::KA;              // A_lo (3xTF32 only)
       if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tAL, wbase + bo);
       else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tAL, wbase + bo);
@@ -359,8 +361,6 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     }
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 2);
     post();
-    // warp 0 polls the commit barrier; the other three sleep in bar.sync instead
-    // of spinning on the mbarrier (a spin costs issue slots the other groups use)
     // every warp parks on the commit barrier (suspend-time hint: no spinning)
     ptx::mbar_wait_sleep(&bars->dfull[g], dphase);
     dphase ^= 1;

@@ -17,6 +17,8 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -428,6 +430,41 @@ void convert(D* dst, const S_* src, size_t n) {
   for (size_t i = 0; i < n; ++i) dst[i] = (D)src[i];
 }
 
+// A batch of element-wise conversions (dst[i] = (D)src[i]) spread over host
+// threads when large: the float64 apply() path converts every output of every
+// chunk (HR @ 65,536: 56 M values), which single-threaded costs ~20 ms.
+template <typename D, typename S_>
+struct ConvertJob {
+  D* dst;
+  const S_* src;
+  size_t n;
+};
+template <typename D, typename S_>
+void convert_all(const std::vector<ConvertJob<D, S_>>& jobs) {
+  size_t total = 0;
+  for (const auto& j : jobs) total += j.n;
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = nt > 16 ? 16 : nt;
+  if (total < (1u << 19) || nt < 2) {
+    for (const auto& j : jobs) convert(j.dst, j.src, j.n);
+    return;
+  }
+  const size_t per = (total + nt - 1) / nt;
+  auto work = [&](size_t lo, size_t hi) {      // global element range [lo, hi)
+    size_t base = 0;
+    for (const auto& j : jobs) {
+      const size_t a = lo > base ? lo - base : 0, b = hi - base < j.n ? hi - base : j.n;
+      if (hi > base && a < j.n && a < b) convert(j.dst + a, j.src + a, b - a);
+      base += j.n;
+      if (base >= hi) break;
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t * per, (t + 1) * per < total ? (t + 1) * per : total);
+  work(0, per < total ? per : total);
+  for (auto& t : th) t.join();
+}
+
 template <typename T, typename OutT>
 tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint32_t flags,
                              const OutT* out) {
@@ -472,12 +509,15 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     const size_t r0 = sc.pending_r0, n = sc.pending_rows;
     err_any |= *(int32_t*)(P + err_off);
     if (!direct) {
-      if (o.logits) convert(o.logits + r0 * C, (const float*)(P + L.logits), n * C);
-      if (o.probabilities) convert(o.probabilities + r0 * C, (const float*)(P + L.probs), n * C);
+      using OutF = std::remove_pointer_t<decltype(o.logits)>;
+      std::vector<ConvertJob<OutF, float>> jobs;
+      if (o.logits) jobs.push_back({o.logits + r0 * C, (const float*)(P + L.logits), n * C});
+      if (o.probabilities) jobs.push_back({o.probabilities + r0 * C, (const float*)(P + L.probs), n * C});
       if (o.masks)
         for (size_t s = 0; s < S; ++s)
-          convert(o.masks + (s * rows + r0) * F, (const float*)(P + L.masks) + s * n * F, n * F);
-      if (o.importance) convert(o.importance + r0 * F, (const float*)(P + L.imp), n * F);
+          jobs.push_back({o.masks + (s * rows + r0) * F, (const float*)(P + L.masks) + s * n * F, n * F});
+      if (o.importance) jobs.push_back({o.importance + r0 * F, (const float*)(P + L.imp), n * F});
+      convert_all(jobs);
       if (o.predicted_class) std::memcpy(o.predicted_class + r0, P + L.pred, n * 4);
     }
     sc.pending_r0 = -1;
@@ -496,7 +536,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     if (direct) {
       TBN_CUDA(cudaMemcpyAsync(D + L.x, (const float*)x + r0 * F, n * F * 4, cudaMemcpyHostToDevice, cs));
     } else {
-      convert((float*)(P + L.x), x + r0 * F, n * F);
+      convert_all(std::vector<ConvertJob<float, T>>{{(float*)(P + L.x), x + r0 * F, n * F}});
       TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, n * F * 4, cudaMemcpyHostToDevice, cs));
     }
     tbn_outputs dout{};

@@ -375,6 +375,17 @@ def run_ours(a) -> None:
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": 1e3 * float(te.item()) / e2e_steps,
                "path": "tbn_forward_host (C-ABI, pinned host fp32 buffers, 3-stream chunked H2D/kernel/D2H)"}
+        # the reference's own call shape: TabNetModel.apply on float64 numpy in/out
+        # (network.py:195-267), host conversions included
+        x64 = xnp.astype(np.float64)
+        model.apply(x64)
+        ta = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            model.apply(x64)
+            ta.append(time.perf_counter() - t0)
+        e2e["apply_f64"] = {"value": rows / min(ta), "unit": "rows/s", "ms_per_call": 1e3 * min(ta),
+                            "path": "TabNetModel.apply (float64 numpy in/out, tbn_forward_host_f64)"}
 
     # ---- latency sweep (config 3) ----
     latency = None

@@ -540,21 +540,26 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       bool done = false;
       for (int it = 0; it <= F; ++it) {
         if (!__any_sync(0xffffffffu, !done)) break;
+        // compare the unshifted logits with tau + max (the shift of sparsemax.py:32
+        // folded into the threshold; the sum is shifted back below) and keep two
+        // 32-column TMEM loads in flight
         float2 sa = f2(0.0f, 0.0f), ca = f2(0.0f, 0.0f);
+        const float th = tau + zmax;
 #pragma unroll 1
-        for (int o = 0; o < FS; o += 32) {
-          float z[32];
+        for (int o = 0; o < FS; o += 64) {
+          float z[64];
           tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
+          tmem_load_n<32, 32>(tq + T_ATT + c * FS + o + 32, z);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float z0 = z[i] - zmax, z1 = z[i + 1] - zmax;     // sparsemax.py:32
-            const float2 mk = f2(z0 > tau ? 1.0f : 0.0f, z1 > tau ? 1.0f : 0.0f);
-            sa = __ffma2_rn(mk, f2(z0, z1), sa);
+          for (int i = 0; i < 64; i += 2) {
+            const float2 mk = f2(z[i] > th ? 1.0f : 0.0f, z[i + 1] > th ? 1.0f : 0.0f);
+            sa = __ffma2_rn(mk, f2(z[i], z[i + 1]), sa);
             ca = __fadd2_rn(ca, mk);
           }
         }
-        exchange(make_float4(sa.x + sa.y, ca.x + ca.y, 0.0f, 0.0f), o4);
+        const float cnt_slice = ca.x + ca.y;
+        exchange(make_float4(fmaf(-cnt_slice, zmax, sa.x + sa.y), cnt_slice, 0.0f, 0.0f), o4);
         const float sm = (o4[0].x + o4[1].x) + (o4[2].x + o4[3].x);
         const float cn = (o4[0].y + o4[1].y) + (o4[2].y + o4[3].y);
         if (!done) {

@@ -281,6 +281,11 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
     }
   }
   a.err_flag = err_flag;
+  if (m->tc.kernel == 3) {               // K3 moves rows with 128-bit accesses
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    if (!al16(a.x) || !al16(a.masks) || !al16(a.importance))
+      return fail(TBN_ERR_INVALID_INPUT, "wide-model kernel needs 16-byte aligned x/masks/importance");
+  }
   if (m->tc.scratch_per_cta)             // K3 scratch after the batch-stats block
     a.scratch = (float*)((char*)workspace + 256 +
                          ((flags & TBN_FLAG_BATCH_STATS)

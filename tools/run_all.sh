@@ -1,0 +1,17 @@
+#!/bin/bash
+# Regenerate the round's evidence on ONE B200 (run under gpurun):
+#   bench lines for every BASELINE config/mode -> gpurun_out/f_*.json,
+#   ncu launch list + full capture of the headline kernel (tools/profile.sh),
+#   then copy/summarize here with:  for f in gpurun_out/f_*.json ...; python tools/summarize_profiles.py
+set -e
+TAG=${TAG:-r1x}
+python bench.py                                   > gpurun_out/f_hr_bf16.json
+python bench.py --precision tf32   --no-cpu-baseline > gpurun_out/f_hr_tf32.json
+python bench.py --precision tf32x3 --no-cpu-baseline > gpurun_out/f_hr_x3.json
+python bench.py --config adult                    > gpurun_out/f_adult_bf16.json
+python bench.py --config adult --precision tf32x3 --no-cpu-baseline > gpurun_out/f_adult_x3.json
+python bench.py --config bls                      > gpurun_out/f_bls_bf16.json
+python bench.py --config hr_latency --rows 1024 --latency-sweep --no-cpu-baseline --steps 20 > gpurun_out/f_lat.json
+python bench.py --config wide --rows 262144 --steps 5 --warmup 3 > gpurun_out/f_wide_bf16.json
+python bench.py --impl reference                  > gpurun_out/f_reference.json
+bash tools/profile.sh hr bf16 $TAG

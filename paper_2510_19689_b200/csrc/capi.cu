@@ -355,6 +355,7 @@ namespace {
 
 constexpr int kNumStreams = 3;
 constexpr int64_t kMinChunk = 8192;
+constexpr int64_t kSmallBatch = 32;       // measured break-even vs one DMA per output: ~64 rows
 
 struct StreamCtx {
   cudaStream_t stream = nullptr;
@@ -418,13 +419,15 @@ Layout layout_for(const tbn_model* m, int64_t rows, uint32_t flags) {
   Layout L{};
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  // x | err | outputs: a small batch moves [x, err] in one H2D copy (err
+  // zeroed in the pinned staging) and [err, outputs] in one D2H copy
   L.x = take(R * F * 4);
+  L.err = take(4);
   L.logits = take(R * C * 4);
   L.probs = take(R * C * 4);
   L.masks = take(S * R * F * 4);
   L.imp = take(R * F * 4);
   L.pred = take(R * 4);
-  L.err = take(4);
   L.ws = take(tbn_workspace_bytes(m, rows, flags));
   L.total = o;
   return L;
@@ -450,7 +453,7 @@ void convert_all(const std::vector<ConvertJob<D, S_>>& jobs) {
   for (const auto& j : jobs) total += j.n;
   unsigned nt = std::thread::hardware_concurrency();
   nt = nt > 16 ? 16 : nt;
-  if (total < (1u << 19) || nt < 2) {
+  if (total < (1u << 21) || nt < 2) {      // thread start-up costs ~0.1 ms
     for (const auto& j : jobs) convert(j.dst, j.src, j.n);
     return;
   }
@@ -490,7 +493,10 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     o.predicted_class = nullptr;
   }
   constexpr bool kF32 = sizeof(T) == 4;
-  const bool direct = kF32 && is_pinned(x) && is_pinned(o.logits) && is_pinned(o.probabilities) &&
+  // Small batches (the serving/latency path) always go through the pinned
+  // staging: 3 API calls (H2D, kernel, D2H) beat one DMA per output array.
+  const bool small = rows <= kSmallBatch;
+  const bool direct = !small && kF32 && is_pinned(x) && is_pinned(o.logits) && is_pinned(o.probabilities) &&
                       is_pinned(o.masks) && is_pinned(o.importance) && is_pinned(o.predicted_class);
   // Batch statistics (negative control) need the whole batch in one call.
   int64_t chunk = rows;
@@ -537,12 +543,13 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     char* P = (char*)sc.pin;
     char* D = (char*)sc.dev;
     cudaStream_t cs = sc.stream;
-    TBN_CUDA(cudaMemsetAsync(D + L.err, 0, 4, cs));
     if (direct) {
+      TBN_CUDA(cudaMemsetAsync(D + L.err, 0, 4, cs));
       TBN_CUDA(cudaMemcpyAsync(D + L.x, (const float*)x + r0 * F, n * F * 4, cudaMemcpyHostToDevice, cs));
     } else {
       convert_all(std::vector<ConvertJob<float, T>>{{(float*)(P + L.x), x + r0 * F, n * F}});
-      TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, n * F * 4, cudaMemcpyHostToDevice, cs));
+      *(int32_t*)(P + L.err) = 0;                 // [x | err] in one copy
+      TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, L.err + 4 - L.x, cudaMemcpyHostToDevice, cs));
     }
     tbn_outputs dout{};
     dout.logits = o.logits ? (float*)(D + L.logits) : nullptr;
@@ -563,6 +570,9 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
       if ((fo = (float*)(void*)o.importance)) TBN_CUDA(cudaMemcpyAsync(fo + r0 * F, dout.importance, n * F * 4, cudaMemcpyDeviceToHost, cs));
       if (o.predicted_class) TBN_CUDA(cudaMemcpyAsync(o.predicted_class + r0, dout.predicted_class, n * 4, cudaMemcpyDeviceToHost, cs));
       TBN_CUDA(cudaMemcpyAsync(P + err_off, D + L.err, 4, cudaMemcpyDeviceToHost, cs));
+    } else if (small) {
+      // [err | logits | probs | masks | importance | pred] in one copy
+      TBN_CUDA(cudaMemcpyAsync(P + L.err, D + L.err, L.pred + n * 4 - L.err, cudaMemcpyDeviceToHost, cs));
     } else {
       if (dout.logits) TBN_CUDA(cudaMemcpyAsync(P + L.logits, dout.logits, n * C * 4, cudaMemcpyDeviceToHost, cs));
       if (dout.probabilities) TBN_CUDA(cudaMemcpyAsync(P + L.probs, dout.probabilities, n * C * 4, cudaMemcpyDeviceToHost, cs));

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <unistd.h>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -57,6 +58,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 }  // namespace
 
 struct tbn_model {
+  uint64_t id = 0;             // unique per created model (keys the host path's graph cache)
   tbn_config cfg{};
   bool regression = false;     // TBN_CFG_REGRESSION: identity head, logits only
   int precision = TBN_PREC_TF32X3;
@@ -159,6 +161,8 @@ tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,
   m->cfg = c;
   m->precision = precision;
   m->regression = regression;
+  static std::atomic<uint64_t> next_id{1};
+  m->id = next_id++;
   m->device = device;
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
 
@@ -364,9 +368,22 @@ struct StreamCtx {
   int64_t pending_r0 = -1, pending_rows = 0;   // chunk whose staged outputs await copy-out
 };
 
+// A small batch's [H2D, forward, D2H] sequence captured once as a CUDA graph
+// and replayed (one launch instead of three API calls on the serving path).
+struct SmallGraph {
+  uint64_t model_id;
+  int64_t rows;
+  uint32_t flags, omask;
+  void* pin;
+  void* dev;
+  cudaGraphExec_t exec;
+};
+
 struct HostCtx {
   StreamCtx s[kNumStreams];
+  std::vector<SmallGraph> graphs;     // LRU-ish, capped (kMaxGraphs)
 };
+constexpr size_t kMaxGraphs = 128;
 
 HostCtx* host_ctx(int device) {
   // Per-thread, per-device: apply() is reentrant and 32
@@ -548,8 +565,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
       TBN_CUDA(cudaMemcpyAsync(D + L.x, (const float*)x + r0 * F, n * F * 4, cudaMemcpyHostToDevice, cs));
     } else {
       convert_all(std::vector<ConvertJob<float, T>>{{(float*)(P + L.x), x + r0 * F, n * F}});
-      *(int32_t*)(P + L.err) = 0;                 // [x | err] in one copy
-      TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, L.err + 4 - L.x, cudaMemcpyHostToDevice, cs));
+      *(int32_t*)(P + L.err) = 0;                 // [x | err] in one copy (issued below)
     }
     tbn_outputs dout{};
     dout.logits = o.logits ? (float*)(D + L.logits) : nullptr;
@@ -557,6 +573,46 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     dout.masks = o.masks ? (float*)(D + L.masks) : nullptr;
     dout.importance = o.importance ? (float*)(D + L.imp) : nullptr;
     dout.predicted_class = o.predicted_class ? (int32_t*)(D + L.pred) : nullptr;
+    static const bool no_graphs = getenv("TBN_TRACE") || getenv("TBN_TRACE_MAPPED");
+    if (small && !no_graphs) {
+      // [x|err] H2D, forward, [err|outputs] D2H as one cached CUDA graph
+      const uint32_t omask = (o.logits ? 1u : 0u) | (o.probabilities ? 2u : 0u) | (o.masks ? 4u : 0u) |
+                             (o.importance ? 8u : 0u) | (o.predicted_class ? 16u : 0u);
+      cudaGraphExec_t exec = nullptr;
+      for (const SmallGraph& sg : hc->graphs)
+        if (sg.model_id == m->id && sg.rows == n && sg.flags == flags && sg.omask == omask &&
+            sg.pin == sc.pin && sg.dev == sc.dev) {
+          exec = sg.exec;
+          break;
+        }
+      if (!exec) {
+        TBN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        cudaMemcpyAsync(D + L.x, P + L.x, L.err + 4 - L.x, cudaMemcpyHostToDevice, cs);
+        st = tbn_forward(m, (const float*)(D + L.x), n, flags, &dout, (int32_t*)(D + L.err),
+                         D + L.ws, L.total - L.ws, cs);
+        cudaMemcpyAsync(P + L.err, D + L.err, L.pred + n * 4 - L.err, cudaMemcpyDeviceToHost, cs);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (st != TBN_OK) {
+          if (graph) cudaGraphDestroy(graph);
+          return st;
+        }
+        if (ce != cudaSuccess) return cuda_fail(ce, "small-batch graph capture");
+        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return cuda_fail(ie, "small-batch graph instantiate");
+        if (hc->graphs.size() >= kMaxGraphs) {
+          cudaGraphExecDestroy(hc->graphs.front().exec);
+          hc->graphs.erase(hc->graphs.begin());
+        }
+        hc->graphs.push_back({m->id, n, flags, omask, sc.pin, sc.dev, exec});
+      }
+      TBN_CUDA(cudaGraphLaunch(exec, cs));
+      sc.pending_r0 = r0;
+      sc.pending_rows = n;
+      continue;
+    }
+    if (!direct) TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, L.err + 4 - L.x, cudaMemcpyHostToDevice, cs));
     st = tbn_forward(m, (const float*)(D + L.x), n, flags, &dout, (int32_t*)(D + L.err),
                      D + L.ws, L.total - L.ws, cs);
     if (st != TBN_OK) return st;

@@ -339,3 +339,40 @@ def test_normalized_flag_and_batch_stats(case, precision):
     rh = m.apply(((x - mu) / np.sqrt(var + 1e-8)).astype(np.float32).astype(np.float64), normalized=True)
     np.testing.assert_allclose(rb.probabilities, rh.probabilities, atol=tol)
     assert not np.allclose(rb.probabilities, r.probabilities, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["adult", "hr", "bls", "wide"])
+@pytest.mark.parametrize("precision", ["tf32x3", "tf32", "bf16", "fp32"])
+def test_nonzero_biases_against_oracle(name, precision):
+    """A trained model has nonzero biases in every FC (init_parameters zeroes
+    them, network.py:71-97, so the goldens never exercise them).  The kernels
+    fold the biases into the GEMMs (ones column in A / bias row in B) or add them
+    in the epilogue; check every kernel against the oracle with random biases."""
+    w = W.WORKLOADS[name]
+    if precision == "tf32x3" and name == "wide":
+        pytest.skip("no 3xTF32 instance for the wide shape")
+    if precision == "tf32" and name == "wide":
+        pytest.skip("no tf32 instance for the wide shape")
+    base = W.make_model(name, "trained")
+    rng = np.random.default_rng(11)
+    params = {k: (v + rng.normal(0.0, 0.3, v.shape) if k.endswith("_b") else v) for k, v in base.params.items()}
+    m = P.TabNetModel(config=base.config, params=params, norm_mean=base.norm_mean, norm_var=base.norm_var,
+                      model_version="bias", precision=precision)
+    x = W.make_inputs(w, 256 if name != "wide" else 64).astype(np.float64)
+    ref = O.apply_model(m, x, diagnostics=True)
+    zs, tau = ref["z_shift"], ref["tau"]
+    scale = np.maximum(np.abs(zs).max(axis=2), 1e-300)
+    ref["margin"] = np.abs(zs - tau[..., None]).min(axis=2) / scale
+    p = np.sort(ref["probabilities"], axis=1)
+    ref["top2_gap"] = p[:, -1] - p[:, -2]
+    r = m.apply(x)
+    if precision in EXACT_PRECISIONS:
+        rep = compare(ref, _res_dict(r))
+        assert rep.ok, rep.summary()
+    else:
+        tol = {"tf32": (5e-3, 5e-2, 1e-2), "bf16": (3e-2, 2.5e-1, 5e-2)}[precision]
+        rep = compare(ref, _res_dict(r), delta=0.0, gap=tol[2], rtol=tol[1],
+                      atol={"probabilities": tol[0], "logits": 10 * tol[0]})
+        assert not rep.class_mismatch_rows, rep.summary()
+        assert rep.max_err["probabilities"] < tol[0] and rep.viol["masks"] == 0 and rep.viol["importance"] == 0, \
+            rep.summary()

@@ -376,3 +376,24 @@ def test_nonzero_biases_against_oracle(name, precision):
         assert not rep.class_mismatch_rows, rep.summary()
         assert rep.max_err["probabilities"] < tol[0] and rep.viol["masks"] == 0 and rep.viol["importance"] == 0, \
             rep.summary()
+
+
+@pytest.mark.parametrize("gamma", [1.0, 2.5])
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16"])
+def test_relaxation_gamma(gamma, precision):
+    """gamma (config.py:26) is a runtime scalar of every kernel: prior *= (gamma - m)
+    (network.py:237)."""
+    base = W.make_model("hr", "trained")
+    cfg = P.ModelConfig(feature_count=35, n_classes=2, n_d=16, n_a=16, n_steps=5, gamma=gamma)
+    m = P.TabNetModel(config=cfg, params=base.params, norm_mean=base.norm_mean, norm_var=base.norm_var,
+                      model_version="gamma", precision=precision)
+    x = W.make_inputs(W.WORKLOADS["hr"], 256).astype(np.float64)
+    ref = O.apply_model(m, x)
+    r = m.apply(x)
+    # gamma away from 1.3 moves |z| by up to gamma^S (or shrinks the prior towards
+    # 0), so the check is on values and on the average mask error, not on exact
+    # support sets; a wrong gamma would be off by O(1) everywhere
+    tol, mtol = (1e-4, 1e-5) if precision == "tf32x3" else (3e-2, 1e-2)
+    np.testing.assert_allclose(r.probabilities, ref["probabilities"], atol=tol)
+    assert np.abs(r.masks - ref["masks"]).mean() < mtol
+    assert np.abs(r.importance - ref["importance"]).mean() < mtol

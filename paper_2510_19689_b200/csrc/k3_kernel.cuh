@@ -108,7 +108,7 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "K3 shared-memory plan");
   // global scratch per CTA: prior, agg and (without a masks output) the step's
   // mask, each [128 rows][F] fp32
-  static constexpr size_t SCRATCH_PER_CTA = 3ull * 128 * F * 4;
+  static constexpr size_t SCRATCH_PER_CTA = 2ull * 128 * F * 4 + 128ull * F * 2;   // prior, agg fp32; mask bf16
   static constexpr int THREADS = 512;
 };
 
@@ -190,14 +190,37 @@ __device__ __forceinline__ void st32s(float* p, const float (&v)[32]) {
   for (int i = 0; i < 8; ++i)
     *reinterpret_cast<float4*>(p + 512 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
 }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&b);
+}
+// 32 features as bf16 over a [F/8][128 rows][8] scratch (16 B per row-octet;
+// a row's consecutive octets are 128*8 bf16 apart)
+__device__ __forceinline__ void st32h(uint16_t* p, const float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<uint4*>(p + 1024 * i) =
+        make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+}
+__device__ __forceinline__ void ld32h(const uint16_t* p, float (&v)[32]) {
+  uint4 t[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = *reinterpret_cast<const uint4*>(p + 1024 * i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t w[4] = {t[i].x, t[i].y, t[i].z, t[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[8 * i + 2 * j] = __uint_as_float(w[j] << 16);
+      v[8 * i + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+    }
+  }
+}
 __device__ __forceinline__ void st32(float* p, const float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i)
     *reinterpret_cast<float4*>(p + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<const uint32_t*>(&b);
 }
 
 template <class CF>
@@ -223,7 +246,9 @@ tabnet_wide(const Params p, const ForwardArgs a) {
   const size_t sofs = (size_t)(c * FS / 4) * 512 + (size_t)r * 4;
   float* my_prior = prior_s + sofs;
   float* my_agg = agg_s + sofs;
-  float* my_msk = msk_s + sofs;
+  // the step's mask as bf16 (feeds x*m, itself rounded to bf16 for the MMA, and
+  // the agg update) — halves its L2 footprint
+  uint16_t* my_msk = reinterpret_cast<uint16_t*>(msk_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
 
   const int64_t tiles_cta = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const uint32_t nchunks = (uint32_t)(tiles_cta * CF::TILE_CH);
@@ -490,7 +515,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float mv[32], ag[32];
-        ld32s(my_msk + (o / 4) * 512, mv);
+        ld32h(my_msk + (o / 8) * 1024, mv);
         if (agg_zero) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) ag[i] = 0.0f;
@@ -591,7 +616,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
           z[i] = mk;
         }
         st32s(my_prior + (o / 4) * 512, pr);
-        st32s(my_msk + (o / 4) * 512, z);
+        st32h(my_msk + (o / 8) * 1024, z);
         if (mwrite) st32(mrow + o, z);
       }
       if (threadIdx.x == 0) TBN_K3T(1003 + 10 * s, clock64());
@@ -600,7 +625,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float xv[32], mv[32];
-        ld32s(my_msk + (o / 4) * 512, mv);
+        ld32h(my_msk + (o / 8) * 1024, mv);
         xn_chunk(o, xv);
         float pk[16];
 #pragma unroll

@@ -108,7 +108,7 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "K3 shared-memory plan");
   // global scratch per CTA: prior, agg and (without a masks output) the step's
   // mask, each [128 rows][F] fp32
-  static constexpr size_t SCRATCH_PER_CTA = 2ull * 128 * F * 4 + 128ull * F * 2;   // prior, agg fp32; mask bf16
+  static constexpr size_t SCRATCH_PER_CTA = 128ull * F * 4 + 2ull * 128 * F * 2;   // prior fp32; agg, mask bf16
   static constexpr int THREADS = 512;
 };
 
@@ -240,12 +240,12 @@ tabnet_wide(const Params p, const ForwardArgs a) {
   const bool issuer = (warp == 0);                   // converged warp; elected lane inside the asm
   float* prior_s = a.scratch + (size_t)blockIdx.x * (CF::SCRATCH_PER_CTA / 4);
   float* agg_s = prior_s + 128 * F;
-  float* msk_s = agg_s + 128 * F;
+  float* msk_s = agg_s + 128 * F / 2;
   // scratch layout [F/4][128][4]: feature f of row r at ((f/4)*128 + r)*4 + f%4;
   // my_*(o) = this thread's 32-feature run starting at slice feature o
   const size_t sofs = (size_t)(c * FS / 4) * 512 + (size_t)r * 4;
   float* my_prior = prior_s + sofs;
-  float* my_agg = agg_s + sofs;
+  uint16_t* my_agg = reinterpret_cast<uint16_t*>(agg_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
   // the step's mask as bf16 (feeds x*m, itself rounded to bf16 for the MMA, and
   // the agg update) — halves its L2 footprint
   uint16_t* my_msk = reinterpret_cast<uint16_t*>(msk_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
@@ -520,11 +520,11 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) ag[i] = 0.0f;
         } else {
-          ld32s(my_agg + (o / 4) * 512, ag);
+          ld32h(my_agg + (o / 8) * 1024, ag);
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) ag[i] = fmaf(agg_w, mv[i], ag[i]);
-        st32s(my_agg + (o / 4) * 512, ag);
+        st32h(my_agg + (o / 8) * 1024, ag);
       }
     };
 
@@ -696,7 +696,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float ag[32];
-        ld32s(my_agg + (o / 4) * 512, ag);
+        ld32h(my_agg + (o / 8) * 1024, ag);
 #pragma unroll
         for (int i = 0; i < 32; ++i) t0 += ag[i];
       }
@@ -709,7 +709,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
         for (int o = 0; o < FS; o += 32) {
           float ag[32];
-          ld32s(my_agg + (o / 4) * 512, ag);
+          ld32h(my_agg + (o / 8) * 1024, ag);
 #pragma unroll
           for (int i = 0; i < 32; ++i) ag[i] *= rdiv;
           st32(irow + o, ag);

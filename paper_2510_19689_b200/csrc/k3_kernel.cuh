@@ -108,7 +108,7 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "K3 shared-memory plan");
   // global scratch per CTA: prior, agg and (without a masks output) the step's
   // mask, each [128 rows][F] fp32
-  static constexpr size_t SCRATCH_PER_CTA = 128ull * F * 4 + 2ull * 128 * F * 2;   // prior fp32; agg, mask bf16
+  static constexpr size_t SCRATCH_PER_CTA = 128ull * F * 4 + 3ull * 128 * F * 2;   // prior fp32; agg, mask, xn bf16
   static constexpr int THREADS = 512;
 };
 
@@ -249,6 +249,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
   // the step's mask as bf16 (feeds x*m, itself rounded to bf16 for the MMA, and
   // the agg update) — halves its L2 footprint
   uint16_t* my_msk = reinterpret_cast<uint16_t*>(msk_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
+  uint16_t* my_xn = my_msk + 128 * F;               // the tile's normalized x (bf16): x*m is bf16 anyway
 
   const int64_t tiles_cta = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const uint32_t nchunks = (uint32_t)(tiles_cta * CF::TILE_CH);
@@ -496,6 +497,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = __uint_as_float(pack_bf16(xv[2 * i], xv[2 * i + 1]));
         tmem_store_n<16>(tq + T_A + (c * FS + o) / 2, pk);
+        st32h(my_xn + (o / 8) * 1024, xv);
       }
       if (bad && a.err_flag) atomicOr(a.err_flag, 1);
     }
@@ -626,7 +628,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       for (int o = 0; o < FS; o += 32) {
         float xv[32], mv[32];
         ld32h(my_msk + (o / 8) * 1024, mv);
-        xn_chunk(o, xv);
+        ld32h(my_xn + (o / 8) * 1024, xv);
         float pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = __uint_as_float(pack_bf16(mv[2 * i] * xv[2 * i], mv[2 * i + 1] * xv[2 * i + 1]));

@@ -108,7 +108,7 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "K3 shared-memory plan");
   // global scratch per CTA: prior, agg and (without a masks output) the step's
   // mask, each [128 rows][F] fp32
-  static constexpr size_t SCRATCH_PER_CTA = 128ull * F * 4 + 3ull * 128 * F * 2;   // prior fp32; agg, mask, xn bf16
+  static constexpr size_t SCRATCH_PER_CTA = 4ull * 128 * F * 2;   // prior, agg, mask, xn: bf16
   static constexpr int THREADS = 512;
 };
 
@@ -239,12 +239,12 @@ tabnet_wide(const Params p, const ForwardArgs a) {
   const uint32_t sbase = ptx::smem_u32(smem);
   const bool issuer = (warp == 0);                   // converged warp; elected lane inside the asm
   float* prior_s = a.scratch + (size_t)blockIdx.x * (CF::SCRATCH_PER_CTA / 4);
-  float* agg_s = prior_s + 128 * F;
+  float* agg_s = prior_s + 128 * F / 2;
   float* msk_s = agg_s + 128 * F / 2;
   // scratch layout [F/4][128][4]: feature f of row r at ((f/4)*128 + r)*4 + f%4;
   // my_*(o) = this thread's 32-feature run starting at slice feature o
   const size_t sofs = (size_t)(c * FS / 4) * 512 + (size_t)r * 4;
-  float* my_prior = prior_s + sofs;
+  uint16_t* my_prior = reinterpret_cast<uint16_t*>(prior_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
   uint16_t* my_agg = reinterpret_cast<uint16_t*>(agg_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
   // the step's mask as bf16 (feeds x*m, itself rounded to bf16 for the MMA, and
   // the agg update) — halves its L2 footprint
@@ -539,7 +539,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
-        if (s > 1) ld32s(my_prior + (o / 4) * 512, pr);   // in flight with the TMEM load
+        if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr);   // in flight with the TMEM load
         tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
         ptx::tmem_ld_wait();
         if (s > 1) {
@@ -608,7 +608,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
-        if (s > 1) ld32s(my_prior + (o / 4) * 512, pr);
+        if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr);
         tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
         ptx::tmem_ld_wait();
 #pragma unroll
@@ -617,7 +617,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
           pr[i] = (s > 1 ? pr[i] : 1.0f) * (p.gamma - mk);                   // network.py:237
           z[i] = mk;
         }
-        st32s(my_prior + (o / 4) * 512, pr);
+        st32h(my_prior + (o / 8) * 1024, pr);
         st32h(my_msk + (o / 8) * 1024, z);
         if (mwrite) st32(mrow + o, z);
       }

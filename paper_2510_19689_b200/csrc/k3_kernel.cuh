@@ -103,7 +103,9 @@ struct Cfg {
   static constexpr int AATT_BYTES = 128 * KATT * 2;
   static constexpr int OFF_CONST = rup(OFF_AATT + AATT_BYTES, 128);
   static constexpr int OFF_XCH = rup(OFF_CONST + CONST_BYTES, 128);   // [4 q][4 c][32 lanes] float4
-  static constexpr int OFF_BAR = OFF_XCH + 2 * 4 * 4 * 32 * 16;   // double-buffered
+  static constexpr int OFF_STG = OFF_XCH + 2 * 4 * 4 * 32 * 16;   // double-buffered
+  static constexpr int STG_WARP = 32 * 16 * 4;     // a warp's 32 rows x 16 features fp32
+  static constexpr int OFF_BAR = OFF_STG + 16 * STG_WARP;
   static constexpr int SMEM_BYTES = OFF_BAR + 256;
   static_assert(SMEM_BYTES <= 227 * 1024, "K3 shared-memory plan");
   // global scratch per CTA: prior, agg and (without a masks output) the step's
@@ -196,17 +198,46 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 // 32 features as bf16 over a [F/8][128 rows][8] scratch (16 B per row-octet;
 // a row's consecutive octets are 128*8 bf16 apart)
-__device__ __forceinline__ void st32h(uint16_t* p, const float (&v)[32]) {
+// The scratch is re-read every step and must survive the streaming outputs
+// (masks/importance, ~18 KB per row) in L2: its accesses carry an evict_last
+// policy and the output stores are streaming (st.global.cs).
+#ifndef TBN_K3_L2HINT
+#define TBN_K3_L2HINT 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void sth4(uint16_t* p, uint4 v, uint64_t pol) {
+#if TBN_K3_L2HINT
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+#else
+  *reinterpret_cast<uint4*>(p) = v;
+#endif
+}
+__device__ __forceinline__ uint4 ldh4(const uint16_t* p, uint64_t pol) {
+#if TBN_K3_L2HINT
+  uint4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol) : "memory");
+  return v;
+#else
+  return *reinterpret_cast<const uint4*>(p);
+#endif
+}
+__device__ __forceinline__ void st32h(uint16_t* p, const float (&v)[32], uint64_t pol) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    *reinterpret_cast<uint4*>(p + 1024 * i) =
-        make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+    sth4(p + 1024 * i,
+         make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                    pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7])), pol);
 }
-__device__ __forceinline__ void ld32h(const uint16_t* p, float (&v)[32]) {
+__device__ __forceinline__ void ld32h(const uint16_t* p, float (&v)[32], uint64_t pol) {
   uint4 t[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) t[i] = *reinterpret_cast<const uint4*>(p + 1024 * i);
+  for (int i = 0; i < 4; ++i) t[i] = ldh4(p + 1024 * i, pol);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t w[4] = {t[i].x, t[i].y, t[i].z, t[i].w};
@@ -216,11 +247,6 @@ __device__ __forceinline__ void ld32h(const uint16_t* p, float (&v)[32]) {
       v[8 * i + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
     }
   }
-}
-__device__ __forceinline__ void st32(float* p, const float (&v)[32]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    *reinterpret_cast<float4*>(p + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
 }
 
 template <class CF>
@@ -241,15 +267,39 @@ tabnet_wide(const Params p, const ForwardArgs a) {
   float* prior_s = a.scratch + (size_t)blockIdx.x * (CF::SCRATCH_PER_CTA / 4);
   float* agg_s = prior_s + 128 * F / 2;
   float* msk_s = agg_s + 128 * F / 2;
-  // scratch layout [F/4][128][4]: feature f of row r at ((f/4)*128 + r)*4 + f%4;
+  // scratch layout (bf16) [F/8][128][8]: feature f of row r at ((f/8)*128 + r)*8 + f%8;
   // my_*(o) = this thread's 32-feature run starting at slice feature o
-  const size_t sofs = (size_t)(c * FS / 4) * 512 + (size_t)r * 4;
+  const uint64_t pol = l2_evict_last();
   uint16_t* my_prior = reinterpret_cast<uint16_t*>(prior_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
   uint16_t* my_agg = reinterpret_cast<uint16_t*>(agg_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
   // the step's mask as bf16 (feeds x*m, itself rounded to bf16 for the MMA, and
   // the agg update) — halves its L2 footprint
   uint16_t* my_msk = reinterpret_cast<uint16_t*>(msk_s) + (size_t)(c * FS / 8) * 1024 + (size_t)r * 8;
   uint16_t* my_xn = my_msk + 128 * F;               // the tile's normalized x (bf16): x*m is bf16 anyway
+
+  // Row-major outputs (masks, importance): a thread holds 32 features of its
+  // own row, so direct stores touch 32 rows (lines) per warp instruction.  The
+  // warp transposes through its SMEM stage, 16 features at a time (XOR-swizzled
+  // float4 slots, conflict-free both ways), and stores 8 rows x 64 B per
+  // instruction.  gbase = this warp's first row at the run's first feature.
+  float4* stg = reinterpret_cast<float4*>(smem + CF::OFF_STG + warp * CF::STG_WARP);
+  auto out32 = [&](float* gbase, int nvalid, const float (&v)[32]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        stg[lane * 4 + (i ^ ((lane >> 1) & 3))] =
+            make_float4(v[16 * h + 4 * i], v[16 * h + 4 * i + 1], v[16 * h + 4 * i + 2], v[16 * h + 4 * i + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rr = j * 8 + (lane >> 2), qq = lane & 3;
+        const float4 t = stg[rr * 4 + (qq ^ ((rr >> 1) & 3))];
+        if (rr < nvalid) __stcs(reinterpret_cast<float4*>(gbase + (int64_t)rr * F + 16 * h + 4 * qq), t);
+      }
+      __syncwarp();
+    }
+  };
 
   const int64_t tiles_cta = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const uint32_t nchunks = (uint32_t)(tiles_cta * CF::TILE_CH);
@@ -465,6 +515,8 @@ tabnet_wide(const Params p, const ForwardArgs a) {
     const int64_t r0 = tile * 128;
     const int64_t row = r0 + r;
     const bool valid = row < a.rows;
+    const int64_t wrow0 = r0 + q * 32;               // this warp's first row
+    const int wvalid = a.rows - wrow0 < 32 ? (int)(a.rows - wrow0) : 32;   // may be <= 0
     const float* xrow = a.x + (valid ? row : 0) * F + c * FS;
 
     // xn slice from x (network.py:118-120): this slice's 128 features
@@ -497,7 +549,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = __uint_as_float(pack_bf16(xv[2 * i], xv[2 * i + 1]));
         tmem_store_n<16>(tq + T_A + (c * FS + o) / 2, pk);
-        st32h(my_xn + (o / 8) * 1024, xv);
+        st32h(my_xn + (o / 8) * 1024, xv, pol);
       }
       if (bad && a.err_flag) atomicOr(a.err_flag, 1);
     }
@@ -517,16 +569,16 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float mv[32], ag[32];
-        ld32h(my_msk + (o / 8) * 1024, mv);
+        ld32h(my_msk + (o / 8) * 1024, mv, pol);
         if (agg_zero) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) ag[i] = 0.0f;
         } else {
-          ld32h(my_agg + (o / 8) * 1024, ag);
+          ld32h(my_agg + (o / 8) * 1024, ag, pol);
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) ag[i] = fmaf(agg_w, mv[i], ag[i]);
-        st32h(my_agg + (o / 8) * 1024, ag);
+        st32h(my_agg + (o / 8) * 1024, ag, pol);
       }
     };
 
@@ -539,7 +591,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
-        if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr);   // in flight with the TMEM load
+        if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr, pol);   // in flight with the TMEM load
         tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
         ptx::tmem_ld_wait();
         if (s > 1) {
@@ -603,12 +655,11 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       // output (or the scratch when none is requested), read back below
       // the mask goes to the coalesced scratch (read back for x*m and the agg
       // update) and, when requested, to the masks output
-      float* mrow = a.masks ? a.masks + ((int64_t)(s - 1) * a.rows + (valid ? row : 0)) * F + c * FS : nullptr;
-      const bool mwrite = a.masks && valid;
+      float* mrow = a.masks ? a.masks + ((int64_t)(s - 1) * a.rows + wrow0) * F + c * FS : nullptr;
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
-        if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr);
+        if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr, pol);
         tmem_load_n<32>(tq + T_ATT + c * FS + o, z);
         ptx::tmem_ld_wait();
 #pragma unroll
@@ -617,9 +668,9 @@ tabnet_wide(const Params p, const ForwardArgs a) {
           pr[i] = (s > 1 ? pr[i] : 1.0f) * (p.gamma - mk);                   // network.py:237
           z[i] = mk;
         }
-        st32h(my_prior + (o / 8) * 1024, pr);
-        st32h(my_msk + (o / 8) * 1024, z);
-        if (mwrite) st32(mrow + o, z);
+        st32h(my_prior + (o / 8) * 1024, pr, pol);
+        st32h(my_msk + (o / 8) * 1024, z, pol);
+        if (mrow) out32(mrow + o, wvalid, z);
       }
       if (threadIdx.x == 0) TBN_K3T(1003 + 10 * s, clock64());
       ptx::named_bar_sync(qbar, 128);                // every slice of the quarter is done with z
@@ -627,8 +678,8 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float xv[32], mv[32];
-        ld32h(my_msk + (o / 8) * 1024, mv);
-        ld32h(my_xn + (o / 8) * 1024, xv);
+        ld32h(my_msk + (o / 8) * 1024, mv, pol);
+        ld32h(my_xn + (o / 8) * 1024, xv, pol);
         float pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = __uint_as_float(pack_bf16(mv[2 * i] * xv[2 * i], mv[2 * i + 1] * xv[2 * i + 1]));
@@ -698,7 +749,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
 #pragma unroll 1
       for (int o = 0; o < FS; o += 32) {
         float ag[32];
-        ld32h(my_agg + (o / 8) * 1024, ag);
+        ld32h(my_agg + (o / 8) * 1024, ag, pol);
 #pragma unroll
         for (int i = 0; i < 32; ++i) t0 += ag[i];
       }
@@ -706,15 +757,15 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       exchange(make_float4(t0, 0.0f, 0.0f, 0.0f), o4);
       const float div = all_eta_zero ? (float)S : (o4[0].x + o4[1].x) + (o4[2].x + o4[3].x);
       const float rdiv = __frcp_rn(div);
-      if (a.importance && valid) {
-        float* irow = a.importance + row * F + c * FS;
+      if (a.importance) {
+        float* irow = a.importance + wrow0 * F + c * FS;
 #pragma unroll 1
         for (int o = 0; o < FS; o += 32) {
           float ag[32];
-          ld32h(my_agg + (o / 8) * 1024, ag);
+          ld32h(my_agg + (o / 8) * 1024, ag, pol);
 #pragma unroll
           for (int i = 0; i < 32; ++i) ag[i] *= rdiv;
-          st32(irow + o, ag);
+          out32(irow + o, wvalid, ag);
         }
       }
     }

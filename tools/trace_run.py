@@ -10,7 +10,8 @@ prec = sys.argv[1] if len(sys.argv) > 1 else "tf32x3"
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 cfg = sys.argv[3] if len(sys.argv) > 3 else "hr"
 m = W.make_engine_model(cfg, "trained", precision=prec, device=0)
-r = DeviceRunner(m, rows, device=0)
+outs = tuple(os.environ.get("TBN_OUTPUTS", "logits,probabilities,masks,importance,predicted_class").split(","))
+r = DeviceRunner(m, rows, device=0, outputs=outs)
 x = torch.from_numpy(W.make_inputs(W.WORKLOADS[cfg], rows)).cuda()
 r.run(x); torch.cuda.synchronize()
 r.run(x); torch.cuda.synchronize()

@@ -139,6 +139,13 @@ tbn_status tbn_sparsemax(const float* z, int64_t rows, int32_t n, float* out,
 /* Host-buffer sparsemax (float64 in/out, computed on device in fp32). */
 tbn_status tbn_sparsemax_host_f64(const double* z, int64_t rows, int32_t n, double* out);
 
+/* Per-partition column means on device: values (partitions*rows_per_partition,
+ * width) fp32, out (partitions, width) float64 (fixed-order fp64 sums).  The
+ * per-batch mean importance of stability_score (interpret/stability.py:103-106)
+ * over one forward of all partitions' rows. */
+tbn_status tbn_partition_mean(const float* values, int64_t rows_per_partition, int32_t partitions,
+                              int32_t width, double* out, void* stream);
+
 /* CRC-32C (Castagnoli, reflected 0x82F63B78) as io.py:22-36, hardware
  * accelerated on the host CPU when SSE4.2 is present.  Pure host code. */
 uint32_t tbn_crc32c(const uint8_t* data, size_t n, uint32_t crc);

@@ -29,7 +29,7 @@ EXPORTED = (
     "tbn_abi_version", "tbn_last_error", "tbn_device_count", "tbn_model_create",
     "tbn_model_destroy", "tbn_model_info", "tbn_workspace_bytes", "tbn_forward",
     "tbn_forward_host", "tbn_forward_host_f64", "tbn_sparsemax",
-    "tbn_sparsemax_host_f64", "tbn_crc32c",
+    "tbn_sparsemax_host_f64", "tbn_partition_mean", "tbn_crc32c",
 )
 
 
@@ -84,6 +84,8 @@ def lib() -> C.CDLL:
         L.tbn_forward_host_f64.argtypes = [vp, vp, i64, u32, C.POINTER(TbnOutputs)]
         L.tbn_sparsemax.restype = i32
         L.tbn_sparsemax.argtypes = [vp, i64, i32, vp, vp]
+        L.tbn_partition_mean.restype = i32
+        L.tbn_partition_mean.argtypes = [vp, i64, i32, i32, vp, vp]
         L.tbn_sparsemax_host_f64.restype = i32
         L.tbn_sparsemax_host_f64.argtypes = [vp, i64, i32, vp]
         L.tbn_crc32c.restype = u32

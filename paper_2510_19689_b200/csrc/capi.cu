@@ -679,6 +679,16 @@ tbn_status tbn_sparsemax(const float* z, int64_t rows, int32_t n, float* out, vo
   return TBN_OK;
 }
 
+tbn_status tbn_partition_mean(const float* v, int64_t per, int32_t partitions, int32_t width,
+                              double* out, void* stream) {
+  if (per < 1 || partitions < 1 || width < 1)
+    return fail(TBN_ERR_INVALID_INPUT, "partition_mean needs rows_per_partition, partitions, width >= 1");
+  if (!v || !out) return fail(TBN_ERR_INVALID_INPUT, "null buffer");
+  cudaError_t e = tbn::launch_partition_mean(v, per, partitions, width, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "partition_mean launch");
+  return TBN_OK;
+}
+
 tbn_status tbn_sparsemax_host_f64(const double* z, int64_t rows, int32_t n, double* out) {
   if (rows < 1 || n < 1) return fail(TBN_ERR_INVALID_INPUT, "sparsemax input must have length >= 1");
   if (n > 512) return fail(TBN_ERR_UNSUPPORTED, "sparsemax width > 512");

@@ -40,7 +40,34 @@ __global__ void batch_stats_kernel(const float* __restrict__ x, int64_t rows, in
   }
 }
 
+// Per-partition column means (stability.py:103-106: each partition's
+// importance.mean(axis=0)): values (P*per, W) fp32 row-major, out (P, W) f64.
+// Block = 32 columns x 8 row lanes; a warp reads 128 contiguous bytes of one
+// row; float64 accumulation, fixed summation order (deterministic).
+__global__ void partition_mean_kernel(const float* __restrict__ v, int64_t per, int W,
+                                      double* __restrict__ out) {
+  __shared__ double red[8][33];
+  const int p = blockIdx.x, f = blockIdx.y * 32 + threadIdx.x;
+  const float* base = v + (int64_t)p * per * W;
+  double s = 0.0;
+  if (f < W)
+    for (int64_t r = threadIdx.y; r < per; r += 8) s += (double)base[r * W + f];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && f < W) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
+    out[(int64_t)p * W + f] = t / (double)per;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_partition_mean(const float* v, int64_t per, int partitions, int W, double* out,
+                                  cudaStream_t stream) {
+  partition_mean_kernel<<<dim3(partitions, (W + 31) / 32), dim3(32, 8), 0, stream>>>(v, per, W, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_batch_stats(const float* x, int64_t rows, int F, float* scale, float* shift,
                                cudaStream_t stream) {

@@ -40,6 +40,8 @@ size_t simt_smem_bytes(const SimtParams& p);
 cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, cudaStream_t stream);
 cudaError_t launch_sparsemax(const float* z, int64_t rows, int n, float* out, int32_t* err_flag,
                              int num_sms, cudaStream_t stream);
+cudaError_t launch_partition_mean(const float* v, int64_t per, int partitions, int W, double* out,
+                                  cudaStream_t stream);
 cudaError_t launch_batch_stats(const float* x, int64_t rows, int F, float* scale, float* shift,
                                cudaStream_t stream);
 

@@ -1,6 +1,7 @@
-"""Stability consumer (paper_2510_19689_b200/interpret.py) against golden
-vectors of the reference's interpret/stability.py
-(tests/golden/make_stability_golden.py)."""
+"""Explain consumers (paper_2510_19689_b200/interpret.py): stability against
+golden vectors of the reference's interpret/stability.py
+(tests/golden/make_stability_golden.py) and the on-device load-invariance check
+(interpret/invariance.py)."""
 import numpy as np
 import pytest
 
@@ -87,3 +88,29 @@ def test_stability_score_rejects_non_finite():
     x[17, 3] = np.nan
     with pytest.raises(P.InvalidInputError):
         I.stability_score(m, x, 4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,precision,rows,conc,bss", [
+    ("hr", "tf32x3", 300, (1, 32), (1, 256)),
+    ("adult", "bf16", 200, (1, 8), (3, 64)),
+    ("wide", "bf16", 130, (1, 4), (1, 128)),
+])
+def test_load_invariance_check_on_device(cfg, precision, rows, conc, bss):
+    from paper_2510_19689_b200 import workloads as W
+    m = W.make_engine_model(cfg, "trained", precision=precision)
+    x = W.make_inputs(W.WORKLOADS[cfg], rows).astype(np.float64)
+    res = I.load_invariance_check(m, x, concurrency=conc, batch_sizes=bss)
+    assert res.passed and res.first_diff is None and res.detail == ""
+    neg = I.load_invariance_check(m, x, concurrency=conc, batch_sizes=bss, use_batch_stats=True)
+    assert not neg.passed
+    s, f = neg.first_diff
+    assert 0 <= s < rows and 0 <= f < x.shape[1]
+    assert neg.detail.startswith(("mask diff at sample", "importance diff at sample"))
+    # the device explanations are the host apply's values
+    ref = m.apply(x)
+    import torch
+    xd = torch.from_numpy(x.astype(np.float32)).cuda()
+    masks, imp = I._device_explanations(m, xd, 7, 3, 0)
+    np.testing.assert_array_equal(masks.cpu().numpy().astype(np.float64), ref.masks)
+    np.testing.assert_array_equal(imp.cpu().numpy().astype(np.float64), ref.importance)

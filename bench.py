@@ -267,6 +267,10 @@ def run_ours(a) -> None:
     per_set = rows * counts["bytes_per_row"]
     nsets = max(2, int(np.ceil(2.5 * L2_BYTES / per_set)))
     nsets = min(nsets, 8)
+    # small batches (Adult, the latency sweep) cannot rotate past L2 with 8 sets:
+    # flush L2 before every timed step instead and time each step on its own
+    flush_mode = nsets * per_set < 2 * L2_BYTES
+    flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush_mode else None
     xs = [torch.from_numpy(W.make_inputs(w, rows, start=(rank * nsets + i) * rows)).to(dev)
           for i in range(nsets)]
     outs = [runner.alloc_outputs(rows) for _ in range(nsets)]
@@ -319,19 +323,35 @@ def run_ours(a) -> None:
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    if use_graph:
-        big.replay()
-    else:
+    flushed_ms = None
+    if flush_mode:
+        # per step: write 2x L2 (torch fill), then the step between its own events;
+        # the host queues the whole loop behind a device sleep so no launch gap
+        # falls inside an event pair
+        pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(a.steps)]
+        torch.cuda._sleep(int(2_000_000 + 60_000 * a.steps))
         for i in range(a.steps):
+            flush_buf.fill_(i & 0xFF)
+            pairs[i][0].record(stream)
             step_fns[i % nsets]()
-    e1.record(stream)
-    torch.cuda.synchronize()
+            pairs[i][1].record(stream)
+        torch.cuda.synchronize()
+        flushed_ms = [p0.elapsed_time(p1) for p0, p1 in pairs]
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if use_graph:
+            big.replay()
+        else:
+            for i in range(a.steps):
+                step_fns[i % nsets]()
+        e1.record(stream)
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    total_ms = e0.elapsed_time(e1)
+    total_ms = sum(flushed_ms) if flush_mode else e0.elapsed_time(e1)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -348,6 +368,8 @@ def run_ours(a) -> None:
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
     per_step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
+    if flush_mode:
+        per_step_ms = flushed_ms        # cold-L2 per-step device times
 
     # ---- end to end through the C-ABI host call: pinned host in/out, H2D+D2H timed
     e2e = None
@@ -422,12 +444,19 @@ def run_ours(a) -> None:
                        "precision": a.precision, "outputs": ("output value, masks (S,B,F), importance" if w.regression else
                                    "logits, probabilities, masks (S,B,F), importance, class"),
                        "parallelism": f"row-shard x{world} (no collective)",
-                       "l2": f"rotating {nsets} input/output sets = {nsets * per_set / 2**20:.0f} MiB > 126 MiB L2",
+                       "l2": (f"flushed before every timed step (a {2 * L2_BYTES >> 20} MiB write; "
+                              f"{nsets} rotating sets = {nsets * per_set / 2**20:.1f} MiB would fit in L2)"
+                              if flush_mode else
+                              f"rotating {nsets} input/output sets = {nsets * per_set / 2**20:.0f} MiB > 126 MiB L2"),
                        "launch": "python loop" if a.no_graph else
-                       "one CUDA graph of the K fused launches (K steps timed as one replay)"},
+                       ("one single-step CUDA graph replay per step between its own CUDA events "
+                        "(the L2 flush outside them); value = rows x K / sum of step times"
+                        if flush_mode else
+                        "one CUDA graph of the K fused launches (K steps timed as one replay)")},
             "roofline": roof,
             "latency_ms": {"p50": nearest_rank(per_step_ms, 50), "p99": nearest_rank(per_step_ms, 99),
-                           "batch": rows, "kind": "device (CUDA events around each step's single-launch graph replay)"},
+                           "batch": rows, "kind": "device (CUDA events around each step's single-launch graph replay"
+                                                   + (", L2 flushed before each)" if flush_mode else ")")},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": a.steps,
@@ -440,9 +469,15 @@ def run_ours(a) -> None:
         dist.destroy_process_group()
 
 
+def x_dev(local):
+    import torch
+    return torch.device("cuda", local)
+
+
 def latency_sweep(model, local, f):
     """HR shape, batches 1..1024 (BASELINE config 3): nearest-rank p50/p99 of the
-    device-only kernel time and of the end-to-end host call."""
+    device-only kernel time (L2 flushed before each call) and of the end-to-end
+    host call."""
     import torch
     from paper_2510_19689_b200.device import DeviceRunner
     res = {}
@@ -450,6 +485,7 @@ def latency_sweep(model, local, f):
     runner = DeviceRunner(model, 1024, device=local)
     stream = torch.cuda.current_stream()
     w = W.WORKLOADS["hr_latency"]
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=x_dev(local))
     for b in (1, 4, 16, 64, 256, 1024):
         x = torch.from_numpy(W.make_inputs(w, b)).cuda()
         for _ in range(20):
@@ -460,6 +496,7 @@ def latency_sweep(model, local, f):
             # a queued spin keeps the GPU busy while the host enqueues the events
             # and the launch, so e0 -> e1 is device time only (no host overhead)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.fill_(len(dev_ms) & 0xFF)      # cold L2 for every timed call
             torch.cuda._sleep(100_000)
             e0.record(stream)
             runner.run(x)

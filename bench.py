@@ -265,11 +265,7 @@ def run_ours(a) -> None:
     f = w.feature_count
     # rotating input/output sets so the timed region always streams from HBM
     per_set = rows * counts["bytes_per_row"]
-    nsets = max(2, int(np.ceil(2.5 * L2_BYTES / per_set)))
-    nsets = min(nsets, 8)
-    # small batches (Adult, the latency sweep) cannot rotate past L2 with 8 sets:
-    # flush L2 before every timed step instead and time each step on its own
-    flush_mode = nsets * per_set < 2 * L2_BYTES
+    nsets, flush_mode = l2_plan(per_set)
     flush_buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush_mode else None
     xs = [torch.from_numpy(W.make_inputs(w, rows, start=(rank * nsets + i) * rows)).to(dev)
           for i in range(nsets)]
@@ -467,6 +463,15 @@ def run_ours(a) -> None:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def l2_plan(per_set_bytes: int) -> tuple:
+    """(rotating input/output sets, flush_mode) for a step that touches
+    ``per_set_bytes``: rotate over >= 2.5x L2 with at most 8 sets; batches too
+    small for that (Adult, the latency sweep) flush L2 before every timed step
+    and time each step on its own instead."""
+    nsets = min(8, max(2, int(np.ceil(2.5 * L2_BYTES / per_set_bytes))))
+    return nsets, nsets * per_set_bytes < 2 * L2_BYTES
 
 
 def x_dev(local):

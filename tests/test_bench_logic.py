@@ -63,3 +63,15 @@ def test_committed_bench_lines_are_consistent():
         r = d["roofline"]
         assert 0.0 < r["frac"] < 1.0 and r["bound"] in ("hbm", "tensor")
         assert d["warmup"] >= 3 and not d["clocks"]["reasons"]
+
+
+def test_l2_plan_rotates_past_l2_or_flushes(bench):
+    for name, rows in [("hr", 65536), ("bls", 262144), ("wide", 262144), ("adult", 4096), ("hr_latency", 1024)]:
+        per_set = rows * W.algorithmic_counts(W.WORKLOADS[name])["bytes_per_row"]
+        nsets, flush = bench.l2_plan(per_set)
+        assert 2 <= nsets <= 8
+        if flush:
+            assert nsets * per_set < 2 * bench.L2_BYTES
+        else:
+            assert nsets * per_set >= 2 * bench.L2_BYTES      # every step streams from HBM
+        assert flush == (name in ("adult", "hr_latency"))

@@ -193,10 +193,15 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int g = warp >> 2, q = warp & 3;
   const int t = q * 32 + lane;                      // row within the tile == TMEM lane
-  const int64_t ntiles = (a.rows + 127) / 128;
   const bool x_bulk_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0);
-  // this CTA's tiles: blockIdx.x + gridDim.x * m, m = g + NG * round
-  const int64_t tiles_cta = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  // this CTA's rows: a contiguous block of R = ceil(rows / grid) rounded up to 4
+  // rows (16-byte aligned row runs); its tiles are 128-row pieces of it, tile m
+  // = g + NG * round.  Every SM gets the same row count, so the batch's last
+  // partial tile per CTA has whole warps without rows, which skip their math.
+  const int64_t rpc = (((a.rows + gridDim.x - 1) / gridDim.x) + 3) & ~(int64_t)3;
+  const int64_t cta_r0 = (int64_t)blockIdx.x * rpc;
+  const int64_t cta_end = cta_r0 + rpc < a.rows ? cta_r0 + rpc : a.rows;
+  const int64_t tiles_cta = cta_end > cta_r0 ? (cta_end - cta_r0 + 127) / 128 : 0;
   const int64_t rounds = (tiles_cta + NG - 1) / NG;
   const uint32_t nblk = (uint32_t)(rounds * NB);    // ring blocks this CTA streams
 
@@ -275,9 +280,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   };
   // rows of this warp in the tile of group-local index m (0 when past the end)
   auto warp_rows = [&](int64_t m, int64_t& r0w) -> int {
-    const int64_t r0 = ((int64_t)blockIdx.x + (int64_t)gridDim.x * m) * 128;
+    const int64_t r0 = cta_r0 + m * 128;
     r0w = r0 + q * 32;
-    const int64_t n = a.rows - r0w;
+    const int64_t n = cta_end - r0w;
     return m >= tiles_cta || n <= 0 ? 0 : (n > 32 ? 32 : (int)n);
   };
   // stg (32 x F, this warp's rows) -> dst rows [0, nw): bulk store when aligned
@@ -443,14 +448,31 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       }
       break;
     }
-    const int64_t tile = (int64_t)blockIdx.x + (int64_t)gridDim.x * m;
-    const int64_t r0 = tile * 128;
-    const int nrows = (int)(a.rows - r0 < 128 ? a.rows - r0 : 128);
+    const int64_t r0 = cta_r0 + m * 128;
+    const int nrows = (int)(cta_end - r0 < 128 ? cta_end - r0 : 128);
     const int nw = nrows - q * 32 < 0 ? 0 : (nrows - q * 32 > 32 ? 32 : nrows - q * 32);
     const bool valid = lane < nw;
     const int64_t row = r0 + t;
     const int64_t r0w = r0 + q * 32;
     const int64_t rv0 = CF::RING ? k * NB : -1;     // this tile's first ring block
+
+    if (nw == 0) {
+      // no rows for this warp (only in a CTA's last, partial tile; warp 0 of the
+      // group always has rows and issues): keep the group's barrier/MMA protocol
+      // — the same GEMM sequence as below — and skip all the math
+      auto skel = [&](int s) {
+        gemm(0, CF::O_SH1, -1, nopost);
+        gemm(1, CF::O_SH2, -1, nopost);
+        gemm(1, CF::O_FC1 + (uint32_t)s * CF::HBR, CF::RING ? rv0 + 2 * s : -1, nopost);
+        gemm(1, CF::O_FC2 + (uint32_t)s * CF::HBR, CF::RING ? rv0 + 2 * s + 1 : -1, nopost);
+      };
+      skel(0);
+      for (int s = 1; s <= S; ++s) {
+        gemm(2, CF::S_ATT + (uint32_t)(s - 1) * CF::ABR, -1, nopost);
+        skel(s);
+      }
+      continue;
+    }
 
     // ---- x -> xn (network.py:118-120), prior = 1, agg = 0 ----
     if (tr) TBN_TRACE(g * 4000 + 3000 + 8 * (int)k);

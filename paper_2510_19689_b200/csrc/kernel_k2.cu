@@ -13,6 +13,10 @@
 #include "k2_kernel.cuh"
 #include "pack_util.h"
 
+#ifndef TBN_K2_ROWQ
+#define TBN_K2_ROWQ 128
+#endif
+
 namespace tbn {
 
 namespace {
@@ -80,8 +84,11 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int64_t ntiles = (a.rows + 127) / 128;
-  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  // one CTA per SM, each with a contiguous, equal block of rows (k2_kernel.cuh);
+  // small batches: one CTA per TBN_K2_ROWQ rows (spreading them thinner, 32
+  // rows per CTA, measured no faster)
+  const int64_t nq = (a.rows + TBN_K2_ROWQ - 1) / TBN_K2_ROWQ;
+  const int grid = (int)(nq < num_sms ? nq : num_sms);
   k2::tabnet_rowthread<CF><<<grid, CF::THREADS, CF::SMEM_BYTES, stream>>>(*(const k2::Params*)m.params, a);
   return cudaGetLastError();
 }

@@ -39,6 +39,8 @@ sustained = 2 * n ** 3 * cnt / (e0.elapsed_time(e1) / 1e3) / 1e12
 out = {"tf32_tflops": burst, "tf32_tflops_sustained": sustained,
        "how": "torch.matmul fp32 8192^3 with allow_tf32 (cuBLAS): best of 10 (burst) and back to back for 4 s (sustained)",
        "gpu": torch.cuda.get_device_name(0)}
-Path("profiles").mkdir(exist_ok=True)
-Path("profiles/measured_tf32.json").write_text(json.dumps(out, indent=1) + "\n")
+# under gpurun only gpurun_out/ comes back: write there too and copy it into profiles/
+for d in ("profiles", "gpurun_out"):
+    Path(d).mkdir(exist_ok=True)
+    Path(d, "measured_tf32.json").write_text(json.dumps(out, indent=1) + "\n")
 print(json.dumps(out))

@@ -444,3 +444,31 @@ def test_sampled_parity_at_full_size(name, precision):
     print(name, precision, len(idx), "rows", rep.summary())
     np.testing.assert_allclose(got["masks"].sum(axis=2), 1.0, atol=1e-4)
     np.testing.assert_allclose(got["importance"].sum(axis=1), 1.0, atol=1e-4)
+
+
+@pytest.mark.parametrize("name,precision", [("hr", "bf16"), ("hr", "tf32x3"), ("bls", "bf16"),
+                                            ("adult", "tf32"), ("wide", "bf16")])
+def test_row_partition_geometry_bitwise(name, precision):
+    """Every batch size maps rows to CTAs, tiles and warps differently (equal
+    contiguous row blocks per CTA, partial last tiles, warps without rows):
+    the outputs of each row must not depend on it.  Odd sizes around the tile,
+    warp and per-CTA boundaries, on the device path, against 1,000-row calls."""
+    import torch
+    from paper_2510_19689_b200.device import DeviceRunner
+    m = P.TabNetModel.from_reference(W.make_model(name), precision=precision)
+    big = 148 * 444 + 5 if name != "wide" else 148 * 128 + 37
+    x = torch.from_numpy(W.make_inputs(W.WORKLOADS[name], big, seed=99)).cuda()
+    runner = DeviceRunner(m, max_rows=big)
+    ref = {}
+    for c0 in range(0, big, 1000):
+        o = runner.run(x[c0:c0 + 1000].contiguous())
+        for k, v in o.items():
+            ref.setdefault(k, []).append(v.clone())
+    ref = {k: torch.cat(v, dim=1 if k == "masks" else 0) for k, v in ref.items()}
+    for rows in (1, 3, 31, 33, 127, 129, 443, 445, 4097, big):
+        o = runner.run(x[:rows].contiguous())
+        torch.cuda.synchronize()
+        for k, v in o.items():
+            want = ref[k][:, :rows] if k == "masks" else ref[k][:rows]
+            assert torch.equal(v, want), (rows, k)
+    runner.check_finite()

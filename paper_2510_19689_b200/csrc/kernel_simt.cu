@@ -6,6 +6,7 @@
 // Per-row results depend only on the row (fixed per-lane k-ascending FFMA
 // chains, fixed butterfly reductions), never on batch size, warp or block
 // position: the batch-invariance contract of network.py:11-14.
+#include <cstdlib>
 #include "tbn_internal.h"
 #include "tbn_device.cuh"
 
@@ -194,7 +195,232 @@ tabnet_forward_simt(SimtParams p, ForwardArgs a) {
   }
 }
 
+// ---- row-blocked variant: 8 rows per block in lockstep --------------------
+// The GEMVs are done by the whole block for its 8 rows at once: a thread owns
+// output column(s) n and accumulates them for several rows, so each weight
+// element it loads feeds several rows' FFMA chains (the per-row kernel above
+// reloads every weight for every row and is L1-bound).  Each output is still ONE
+// fp32 FFMA chain over k ascending, then + bias: bit-for-bit the per-row
+// kernel's arithmetic, so outputs are identical (batch invariance holds).
+constexpr int kBR = 8;                                 // rows per block == warps
+
+__device__ __forceinline__ int rup4(int v) { return (v + 3) & ~3; }
+
+struct BlkLayout {   // per-row SMEM buffers, each 16-byte aligned
+  int F4, H4, N4, ND4;
+  int xn, prior, agg, m, msum, in, u, g, dsum, per_row;
+  __device__ __forceinline__ BlkLayout(int F, int H, int ND) {
+    F4 = rup4(F); H4 = rup4(H); N4 = rup4(2 * H); ND4 = rup4(ND);
+    xn = 0; prior = xn + F4; agg = prior + F4; m = agg + F4; msum = m + F4; in = msum + F4;
+    u = in + F4; g = u + N4; dsum = g + H4; per_row = dsum + ND4;
+  }
+};
+
+// out_r[n] = b[n] + sum_k in_r[k] W[k*N + n] for the block's 8 rows.
+// NJ > 0: N = 256*NJ, thread t owns columns t + 256 j for all 8 rows.
+// NJ == 0: N < 256 divides 256, thread t owns column t % N for rows t / N + (256/N) i.
+template <int NJ, int NR>
+__device__ __forceinline__ void blk_gemv(float* smem_rows, int per_row, int in_off, int out_off,
+                                         int K, const float* __restrict__ W,
+                                         const float* __restrict__ b, int N) {
+  const int t = threadIdx.x;
+  constexpr int NC = NJ > 0 ? NJ : 1;                  // columns per thread
+  constexpr int RR = NJ > 0 ? kBR : NR;                // rows per thread
+  int col[NC], row[RR];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) col[j] = NJ > 0 ? t + 256 * j : t % N;
+#pragma unroll
+  for (int i = 0; i < RR; ++i) row[i] = NJ > 0 ? i : t / N + (256 / N) * i;
+  float acc[NC][RR];
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+#pragma unroll
+    for (int i = 0; i < RR; ++i) acc[j][i] = 0.0f;
+  const int K4 = K & ~3;
+  for (int k = 0; k < K4; k += 4) {
+    float w[4][NC];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) w[kk][j] = __ldg(W + (size_t)(k + kk) * N + col[j]);
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+      const float4 a = *reinterpret_cast<const float4*>(smem_rows + row[i] * per_row + in_off + k);
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        acc[j][i] = fmaf(a.x, w[0][j], acc[j][i]);
+        acc[j][i] = fmaf(a.y, w[1][j], acc[j][i]);
+        acc[j][i] = fmaf(a.z, w[2][j], acc[j][i]);
+        acc[j][i] = fmaf(a.w, w[3][j], acc[j][i]);
+      }
+    }
+  }
+  for (int k = K4; k < K; ++k) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const float wv = __ldg(W + (size_t)k * N + col[j]);
+#pragma unroll
+      for (int i = 0; i < RR; ++i) acc[j][i] = fmaf(smem_rows[row[i] * per_row + in_off + k], wv, acc[j][i]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const float bv = __ldg(b + col[j]);
+#pragma unroll
+    for (int i = 0; i < RR; ++i) smem_rows[row[i] * per_row + out_off + col[j]] = acc[j][i] + bv;
+  }
+}
+
+// dispatch on N (2H for the transformer GEMVs, F for the attentive one)
+__device__ __forceinline__ bool blk_gemv_n(float* sm, int per_row, int in_off, int out_off, int K,
+                                           const float* W, const float* b, int N) {
+  switch (N) {
+    case 32: blk_gemv<0, 1>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 64: blk_gemv<0, 2>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 128: blk_gemv<0, 4>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 256: blk_gemv<1, 0>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 512: blk_gemv<2, 0>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    default: return false;
+  }
+}
+
+__device__ __forceinline__ void blk_glu(float* r, const BlkLayout& L, int H, bool residual, int lane) {
+  for (int j = lane; j < H; j += 32) {
+    float v = r[L.u + j] * sigmoid_accurate(r[L.u + H + j]);
+    r[L.g + j] = residual ? (v + r[L.g + j]) * kResidualScale : v;
+  }
+}
+
+// the feature transformer for the block's rows: in (per row at L.in, or xn) -> g
+__device__ __forceinline__ void blk_transform(const SimtParams& p, float* sm, const BlkLayout& L,
+                                              int in_off, int step, float* r, int lane) {
+  const int H = p.H, N = 2 * H;
+  blk_gemv_n(sm, L.per_row, in_off, L.u, p.F, p.sh1_W, p.sh1_b, N);
+  __syncthreads();
+  blk_glu(r, L, H, false, lane);
+  __syncthreads();
+  blk_gemv_n(sm, L.per_row, L.g, L.u, H, p.sh2_W, p.sh2_b, N);
+  __syncthreads();
+  blk_glu(r, L, H, true, lane);
+  __syncthreads();
+  blk_gemv_n(sm, L.per_row, L.g, L.u, H, p.fc1_W + (size_t)step * H * N, p.fc1_b + (size_t)step * N, N);
+  __syncthreads();
+  blk_glu(r, L, H, true, lane);
+  __syncthreads();
+  blk_gemv_n(sm, L.per_row, L.g, L.u, H, p.fc2_W + (size_t)step * H * N, p.fc2_b + (size_t)step * N, N);
+  __syncthreads();
+  blk_glu(r, L, H, true, lane);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBR * 32)
+tabnet_forward_simt_blk(SimtParams p, ForwardArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int F = p.F, ND = p.ND, S = p.S, C = p.C;
+  const BlkLayout L(F, p.H, ND);
+  float* r = smem + warp * L.per_row;                  // this warp's row
+  const float* scale = a.scale ? a.scale : p.scale;
+  const float* shift = a.shift ? a.shift : p.shift;
+
+  for (int64_t r0 = (int64_t)blockIdx.x * kBR; r0 < a.rows; r0 += (int64_t)gridDim.x * kBR) {
+    const int64_t row = r0 + warp;
+    const bool valid = row < a.rows;
+    int bad = 0;
+    for (int f = lane; f < L.F4; f += 32) {
+      float xv = (valid && f < F) ? a.x[row * F + f] : 0.0f;
+      if (valid && f < F) bad |= !isfinite(xv);
+      r[L.xn + f] = (f < F && !a.normalized) ? (xv - shift[f]) * scale[f] : xv;
+      r[L.prior + f] = 1.0f;
+      r[L.agg + f] = 0.0f;
+      r[L.msum + f] = 0.0f;
+      r[L.in + f] = 0.0f;
+    }
+    if (__any_sync(kFull, bad) && lane == 0 && a.err_flag) atomicOr(a.err_flag, 1);
+    for (int j = lane; j < ND; j += 32) r[L.dsum + j] = 0.0f;
+    __syncthreads();
+    blk_transform(p, smem, L, L.xn, 0, r, lane);
+    for (int s = 1; s <= S; ++s) {
+      // att = a @ W_att + b for the block's rows (into m), z = prior * att
+      blk_gemv_n(smem, L.per_row, L.g + ND, L.m, p.NA, p.att_W + (size_t)(s - 1) * p.NA * F,
+                 p.att_b + (size_t)(s - 1) * F, F);
+      __syncthreads();
+      float zs[kFPerLane];
+      float zmax = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kFPerLane; ++i) {
+        const int f = lane + 32 * i;
+        float z = -INFINITY;
+        if (f < F) z = r[L.prior + f] * r[L.m + f];
+        zs[i] = z;
+        zmax = fmaxf(zmax, z);
+      }
+      zmax = warp_max(zmax);
+#pragma unroll
+      for (int i = 0; i < kFPerLane; ++i) zs[i] -= zmax;   // sparsemax.py:32
+      const float tau = warp_sparsemax_tau(zs, F, lane);
+      float* mask_out = (a.masks && valid) ? a.masks + ((size_t)(s - 1) * a.rows + row) * F : nullptr;
+#pragma unroll
+      for (int i = 0; i < kFPerLane; ++i) {
+        const int f = lane + 32 * i;
+        if (f < F) {
+          const float mv = fmaxf(zs[i] - tau, 0.0f);             // sparsemax.py:40
+          r[L.m + f] = mv;
+          r[L.prior + f] = r[L.prior + f] * (p.gamma - mv);      // network.py:237
+          r[L.in + f] = mv * r[L.xn + f];                        // network.py:238
+          if (mask_out) mask_out[f] = mv;                        // network.py:246
+          r[L.msum + f] += mv;
+        }
+      }
+      __syncthreads();
+      blk_transform(p, smem, L, L.in, s, r, lane);
+      float eta = 0.0f;
+      for (int j = lane; j < ND; j += 32) {
+        const float d = fmaxf(r[L.g + j], 0.0f);
+        r[L.dsum + j] += d;
+        eta += d;
+      }
+      eta = warp_sum(eta);
+      for (int f = lane; f < F; f += 32) r[L.agg + f] = fmaf(eta, r[L.m + f], r[L.agg + f]);
+      __syncthreads();
+    }
+    float logit = -INFINITY;
+    if (lane < C) {
+      float acc = 0.0f;
+      for (int k = 0; k < ND; ++k) acc = fmaf(r[L.dsum + k], __ldg(p.head_W + (size_t)k * C + lane), acc);
+      logit = acc + __ldg(p.head_b + lane);
+    }
+    const float lmax = warp_max(logit);
+    const float e = (lane < C) ? expf(logit - lmax) : 0.0f;
+    const float esum = warp_sum(e);
+    const float prob = e / esum;
+    if (valid && lane < C) {
+      if (a.logits) a.logits[row * C + lane] = logit;
+      if (a.probs) a.probs[row * C + lane] = prob;
+    }
+    float bv = (lane < C) ? prob : -INFINITY;
+    int bi = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(kFull, bv, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (valid && lane == 0 && a.pred) a.pred[row] = bi;
+    float tot = 0.0f;
+    for (int f = lane; f < F; f += 32) tot += r[L.agg + f];
+    tot = warp_sum(tot);
+    if (valid && a.importance) {
+      for (int f = lane; f < F; f += 32)
+        a.importance[row * F + f] = (tot > 0.0f) ? r[L.agg + f] / tot : r[L.msum + f] / (float)S;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+static int rup4_host(int v) { return (v + 3) & ~3; }
 
 size_t simt_smem_bytes(const SimtParams& p) {
   return (size_t)kWarpsPerBlock * (5 * p.F + 3 * p.H + p.ND + p.F) * sizeof(float);
@@ -212,6 +438,24 @@ cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, 
   int64_t max_blocks = (int64_t)num_sms * 8;
   int grid = (int)(blocks_needed < max_blocks ? blocks_needed : max_blocks);
   if (grid < 1) grid = 1;
+  static const bool per_row = getenv("TBN_SIMT_PER_ROW") != nullptr;   // A/B: the first kernel
+  const int n2 = 2 * p.H;
+  const bool blk_ok = !per_row && (n2 == 32 || n2 == 64 || n2 == 128 || n2 == 256) &&
+                      (p.F == 32 || p.F == 64 || p.F == 128 || p.F == 256 || p.F == 512) && p.ND % 4 == 0;
+  if (blk_ok) {
+    const int per_row_floats = 6 * rup4_host(p.F) + rup4_host(n2) + rup4_host(p.H) + rup4_host(p.ND);
+    const size_t bsmem = (size_t)kBR * per_row_floats * sizeof(float);
+    static bool bconf = false;
+    if (!bconf) {
+      cudaFuncSetAttribute(tabnet_forward_simt_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      bconf = true;
+    }
+    const int64_t nb = (a.rows + kBR - 1) / kBR;
+    const int64_t cap = (int64_t)num_sms * 4;
+    const int bgrid = (int)(nb < cap ? nb : cap);
+    tabnet_forward_simt_blk<<<bgrid < 1 ? 1 : bgrid, kBR * 32, bsmem, stream>>>(p, a);
+    return cudaGetLastError();
+  }
   tabnet_forward_simt<<<grid, kWarpsPerBlock * 32, smem, stream>>>(p, a);
   return cudaGetLastError();
 }

@@ -195,14 +195,18 @@ tabnet_forward_simt(SimtParams p, ForwardArgs a) {
   }
 }
 
-// ---- row-blocked variant: 8 rows per block in lockstep --------------------
+// ---- row-blocked variant: kBR rows per block in lockstep ------------------
 // The GEMVs are done by the whole block for its 8 rows at once: a thread owns
 // output column(s) n and accumulates them for several rows, so each weight
 // element it loads feeds several rows' FFMA chains (the per-row kernel above
 // reloads every weight for every row and is L1-bound).  Each output is still ONE
 // fp32 FFMA chain over k ascending, then + bias: bit-for-bit the per-row
 // kernel's arithmetic, so outputs are identical (batch invariance holds).
-constexpr int kBR = 8;                                 // rows per block == warps
+#ifndef TBN_SIMT_BR
+#define TBN_SIMT_BR 16
+#endif
+constexpr int kBR = TBN_SIMT_BR;                       // rows per block == warps
+constexpr int kBT = 32 * kBR;                          // threads per block
 
 __device__ __forceinline__ int rup4(int v) { return (v + 3) & ~3; }
 
@@ -216,21 +220,20 @@ struct BlkLayout {   // per-row SMEM buffers, each 16-byte aligned
   }
 };
 
-// out_r[n] = b[n] + sum_k in_r[k] W[k*N + n] for the block's 8 rows.
-// NJ > 0: N = 256*NJ, thread t owns columns t + 256 j for all 8 rows.
-// NJ == 0: N < 256 divides 256, thread t owns column t % N for rows t / N + (256/N) i.
-template <int NJ, int NR>
+// out_r[n] = b[n] + sum_k in_r[k] W[k*N + n] for the block's kBR rows.
+// N >= kBT: thread t owns columns t + kBT j (NC of them) for all rows (RR = kBR);
+// N <  kBT: thread t owns column t % N for rows t / N + (kBT / N) i (RR of them).
+template <int NC, int RR>
 __device__ __forceinline__ void blk_gemv(float* smem_rows, int per_row, int in_off, int out_off,
                                          int K, const float* __restrict__ W,
                                          const float* __restrict__ b, int N) {
   const int t = threadIdx.x;
-  constexpr int NC = NJ > 0 ? NJ : 1;                  // columns per thread
-  constexpr int RR = NJ > 0 ? kBR : NR;                // rows per thread
+  const bool wide_n = N >= kBT;
   int col[NC], row[RR];
 #pragma unroll
-  for (int j = 0; j < NC; ++j) col[j] = NJ > 0 ? t + 256 * j : t % N;
+  for (int j = 0; j < NC; ++j) col[j] = wide_n ? t + kBT * j : t % N;
 #pragma unroll
-  for (int i = 0; i < RR; ++i) row[i] = NJ > 0 ? i : t / N + (256 / N) * i;
+  for (int i = 0; i < RR; ++i) row[i] = wide_n ? i : t / N + (kBT / N) * i;
   float acc[NC][RR];
 #pragma unroll
   for (int j = 0; j < NC; ++j)
@@ -272,14 +275,20 @@ __device__ __forceinline__ void blk_gemv(float* smem_rows, int per_row, int in_o
 }
 
 // dispatch on N (2H for the transformer GEMVs, F for the attentive one)
+template <int T>
+struct GemvShape {
+  static constexpr int nc(int n) { return n >= T ? n / T : 1; }
+  static constexpr int rr(int n) { return n >= T ? kBR : kBR * n / T; }
+};
 __device__ __forceinline__ bool blk_gemv_n(float* sm, int per_row, int in_off, int out_off, int K,
                                            const float* W, const float* b, int N) {
+  using G = GemvShape<kBT>;
   switch (N) {
-    case 32: blk_gemv<0, 1>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 64: blk_gemv<0, 2>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 128: blk_gemv<0, 4>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 256: blk_gemv<1, 0>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 512: blk_gemv<2, 0>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 32: blk_gemv<G::nc(32), G::rr(32)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 64: blk_gemv<G::nc(64), G::rr(64)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 128: blk_gemv<G::nc(128), G::rr(128)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 256: blk_gemv<G::nc(256), G::rr(256)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 512: blk_gemv<G::nc(512), G::rr(512)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
     default: return false;
   }
 }
@@ -313,7 +322,7 @@ __device__ __forceinline__ void blk_transform(const SimtParams& p, float* sm, co
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBR * 32)
+__global__ void __launch_bounds__(kBT)
 tabnet_forward_simt_blk(SimtParams p, ForwardArgs a) {
   extern __shared__ __align__(16) float smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -440,20 +449,23 @@ cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, 
   if (grid < 1) grid = 1;
   static const bool per_row = getenv("TBN_SIMT_PER_ROW") != nullptr;   // A/B: the first kernel
   const int n2 = 2 * p.H;
+  const int per_row_floats = 6 * rup4_host(p.F) + rup4_host(n2) + rup4_host(p.H) + rup4_host(p.ND);
+  const size_t bsmem = (size_t)kBR * per_row_floats * sizeof(float);
   const bool blk_ok = !per_row && (n2 == 32 || n2 == 64 || n2 == 128 || n2 == 256) &&
-                      (p.F == 32 || p.F == 64 || p.F == 128 || p.F == 256 || p.F == 512) && p.ND % 4 == 0;
+                      (p.F == 32 || p.F == 64 || p.F == 128 || p.F == 256 || p.F == 512) &&
+                      p.ND % 4 == 0 && bsmem <= 227 * 1024;
   if (blk_ok) {
-    const int per_row_floats = 6 * rup4_host(p.F) + rup4_host(n2) + rup4_host(p.H) + rup4_host(p.ND);
-    const size_t bsmem = (size_t)kBR * per_row_floats * sizeof(float);
     static bool bconf = false;
     if (!bconf) {
-      cudaFuncSetAttribute(tabnet_forward_simt_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(tabnet_forward_simt_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       bconf = true;
     }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tabnet_forward_simt_blk, kBT, bsmem);
     const int64_t nb = (a.rows + kBR - 1) / kBR;
-    const int64_t cap = (int64_t)num_sms * 4;
+    const int64_t cap = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
     const int bgrid = (int)(nb < cap ? nb : cap);
-    tabnet_forward_simt_blk<<<bgrid < 1 ? 1 : bgrid, kBR * 32, bsmem, stream>>>(p, a);
+    tabnet_forward_simt_blk<<<bgrid < 1 ? 1 : bgrid, kBT, bsmem, stream>>>(p, a);
     return cudaGetLastError();
   }
   tabnet_forward_simt<<<grid, kWarpsPerBlock * 32, smem, stream>>>(p, a);

@@ -472,3 +472,29 @@ def test_row_partition_geometry_bitwise(name, precision):
             want = ref[k][:, :rows] if k == "masks" else ref[k][:rows]
             assert torch.equal(v, want), (rows, k)
     runner.check_finite()
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32x3"])
+def test_host_call_pinned_buffers_graph_replay(precision):
+    """tbn_forward_host with pinned caller buffers (the DMA-direct path, chunked
+    over 3 streams from 16,384 rows): repeated calls with new contents in the same
+    buffers must equal the device path bitwise; non-finite input still raises."""
+    import torch
+    from paper_2510_19689_b200.device import DeviceRunner
+    m = P.TabNetModel.from_reference(W.make_model("hr"), precision=precision)
+    eng = m.engine()
+    runner = DeviceRunner(m, max_rows=20000)
+    for rows in (33, 1000, 8192, 20000):
+        xp = torch.empty((rows, 35), dtype=torch.float32).pin_memory()
+        outs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in runner.views(rows).items()}
+        npo = {k: v.numpy() for k, v in outs.items()}
+        for seed in (1, 2, 3):
+            xp.copy_(torch.from_numpy(W.make_inputs(W.WORKLOADS["hr"], rows, seed=seed)))
+            eng.forward_host_f32(xp.numpy(), 0, npo)
+            ref = runner.run(xp.cuda())
+            torch.cuda.synchronize()
+            for k in npo:
+                assert np.array_equal(npo[k], ref[k].cpu().numpy()), (rows, seed, k)
+        xp[rows // 2, 3] = float("nan")
+        with pytest.raises(P.InvalidInputError):
+            eng.forward_host_f32(xp.numpy(), 0, npo)

@@ -277,8 +277,8 @@ __device__ __forceinline__ void blk_gemv(float* smem_rows, int per_row, int in_o
 // dispatch on N (2H for the transformer GEMVs, F for the attentive one)
 template <int T>
 struct GemvShape {
-  static constexpr int nc(int n) { return n >= T ? n / T : 1; }
-  static constexpr int rr(int n) { return n >= T ? kBR : kBR * n / T; }
+  __host__ __device__ static constexpr int nc(int n) { return n >= T ? n / T : 1; }
+  __host__ __device__ static constexpr int rr(int n) { return n >= T ? kBR : kBR * n / T; }
 };
 __device__ __forceinline__ bool blk_gemv_n(float* sm, int per_row, int in_off, int out_off, int K,
                                            const float* W, const float* b, int N) {

@@ -113,7 +113,9 @@ tbn_status tbn_model_info(const tbn_model* model, tbn_config* cfg,
 /* Device workspace needed by tbn_forward for `rows` rows (>= 256 bytes). */
 size_t tbn_workspace_bytes(const tbn_model* model, int64_t rows, uint32_t flags);
 
-/* Async forward on `stream` (a cudaStream_t; NULL = legacy default stream).
+/* TabNetModel.apply (network.py:195-267) on device: normalize, S+1 feature
+ * transformers, S attentive steps with sparsemax, head/softmax, importance.
+ * Async forward on `stream` (a cudaStream_t; NULL = legacy default stream).
  * x: device float32 (rows, F) row-major.  Outputs are device pointers.
  * A non-finite input sets *err_flag (device int32, may be NULL) to nonzero;
  * the caller checks it after synchronizing (tbn_forward_host does).
@@ -123,7 +125,8 @@ tbn_status tbn_forward(const tbn_model* model, const float* x, int64_t rows,
                        uint32_t flags, const tbn_outputs* out, int32_t* err_flag,
                        void* workspace, size_t workspace_bytes, void* stream);
 
-/* Synchronous host-buffer forward (the reference-facing call): stages x
+/* Synchronous host-buffer forward (the reference-facing call, replacing the
+ * body of TabNetModel.apply network.py:195-267 incl. its validation :204-211): stages x
  * through pinned memory on a per-thread stream, runs tbn_forward, copies the
  * outputs back, and returns TBN_ERR_INVALID_INPUT on non-finite input.
  * Reentrant: safe from many host threads at once. */

@@ -2,7 +2,7 @@
 // models (F = 512 features, h = 128: BASELINE config 5) as one persistent
 // sm_100a kernel, bf16 tcgen05 contractions.
 //
-// Why a third design: a wide row's state (xn, prior, agg: 3 x 512 floats)
+// Why a third design: a wide row's state (xn, prior, agg, mask: 4 x 512 values)
 // fits neither TMEM nor registers, and the model (1M params, 2 MB in bf16)
 // does not fit shared memory.  So K3 keeps ONE 128-row tile per CTA on chip
 // and streams everything else:
@@ -13,7 +13,8 @@
 //            D 256                       consts, shared1 bias, head
 //   hidden: A = g (K=144) 72 | D 256     per-quarter exchange slots
 //
-//   global scratch per CTA (L2-resident): prior [128][F], agg [128][F] fp32
+//   global scratch per CTA (L2-resident, evict_last): xn, prior, agg and the
+//   step's mask, each [F/8][128 rows][8] bf16 (512 KB per CTA at F = 512)
 //
 // 16 warps: warp w owns TMEM lane quarter q = w % 4 (rows 32q..32q+31) and
 // slice c = w / 4: features [128c, 128c+128) and GLU outputs [32c, 32c+32).
@@ -108,9 +109,8 @@ struct Cfg {
   static constexpr int OFF_BAR = OFF_STG + 16 * STG_WARP;
   static constexpr int SMEM_BYTES = OFF_BAR + 256;
   static_assert(SMEM_BYTES <= 227 * 1024, "K3 shared-memory plan");
-  // global scratch per CTA: prior, agg and (without a masks output) the step's
-  // mask, each [128 rows][F] fp32
-  static constexpr size_t SCRATCH_PER_CTA = 4ull * 128 * F * 2;   // prior, agg, mask, xn: bf16
+  // global scratch per CTA: prior, agg, the step's mask and xn, bf16 each
+  static constexpr size_t SCRATCH_PER_CTA = 4ull * 128 * F * 2;
   static constexpr int THREADS = 512;
 };
 

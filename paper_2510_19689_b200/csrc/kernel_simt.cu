@@ -224,7 +224,7 @@ struct BlkLayout {   // per-row SMEM buffers, each 16-byte aligned
 // N >= kBT: thread t owns columns t + kBT j (NC of them) for all rows (RR = kBR);
 // N <  kBT: thread t owns column t % N for rows t / N + (kBT / N) i (RR of them).
 template <int NC, int RR>
-__device__ __forceinline__ void blk_gemv(float* smem_rows, int per_row, int in_off, int out_off,
+__device__ __forceinline__ void blk_gemv_p2(float* smem_rows, int per_row, int in_off, int out_off,
                                          int K, const float* __restrict__ W,
                                          const float* __restrict__ b, int N) {
   const int t = threadIdx.x;
@@ -280,17 +280,80 @@ struct GemvShape {
   __host__ __device__ static constexpr int nc(int n) { return n >= T ? n / T : 1; }
   __host__ __device__ static constexpr int rr(int n) { return n >= T ? kBR : kBR * n / T; }
 };
-__device__ __forceinline__ bool blk_gemv_n(float* sm, int per_row, int in_off, int out_off, int K,
+__device__ __forceinline__ bool blk_gemv_pow2(float* sm, int per_row, int in_off, int out_off, int K,
                                            const float* W, const float* b, int N) {
   using G = GemvShape<kBT>;
   switch (N) {
-    case 32: blk_gemv<G::nc(32), G::rr(32)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 64: blk_gemv<G::nc(64), G::rr(64)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 128: blk_gemv<G::nc(128), G::rr(128)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 256: blk_gemv<G::nc(256), G::rr(256)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
-    case 512: blk_gemv<G::nc(512), G::rr(512)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 32: blk_gemv_p2<G::nc(32), G::rr(32)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 64: blk_gemv_p2<G::nc(64), G::rr(64)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 128: blk_gemv_p2<G::nc(128), G::rr(128)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 256: blk_gemv_p2<G::nc(256), G::rr(256)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
+    case 512: blk_gemv_p2<G::nc(512), G::rr(512)>(sm, per_row, in_off, out_off, K, W, b, N); return true;
     default: return false;
   }
+}
+
+// out_r[n] = b[n] + sum_k in_r[k] W[k*N + n] for the block's kBR rows (N <= kBT).
+// The block's threads form G = kBT / N groups of N: thread t owns column t % N
+// for rows t / N + G i (i < RR = ceil(kBR / G); rows past kBR are skipped).
+template <int RR>
+__device__ __forceinline__ void blk_gemv_any(float* smem_rows, int per_row, int in_off, int out_off,
+                                         int K, const float* __restrict__ W,
+                                         const float* __restrict__ b, int N) {
+  const int t = threadIdx.x;
+  const int G = kBT / N;
+  if (t >= G * N) return;
+  const int col = t % N, rg = t / N;
+  int row[RR];
+  bool ok[RR];
+#pragma unroll
+  for (int i = 0; i < RR; ++i) {
+    row[i] = rg + G * i;
+    ok[i] = row[i] < kBR;
+    if (!ok[i]) row[i] = 0;
+  }
+  float acc[RR];
+#pragma unroll
+  for (int i = 0; i < RR; ++i) acc[i] = 0.0f;
+  const int K4 = K & ~3;
+  for (int k = 0; k < K4; k += 4) {
+    float w[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) w[kk] = __ldg(W + (size_t)(k + kk) * N + col);
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+      if (RR > 1 && !ok[i]) continue;
+      const float4 a = *reinterpret_cast<const float4*>(smem_rows + row[i] * per_row + in_off + k);
+      acc[i] = fmaf(a.x, w[0], acc[i]);
+      acc[i] = fmaf(a.y, w[1], acc[i]);
+      acc[i] = fmaf(a.z, w[2], acc[i]);
+      acc[i] = fmaf(a.w, w[3], acc[i]);
+    }
+  }
+  for (int k = K4; k < K; ++k) {
+    const float wv = __ldg(W + (size_t)k * N + col);
+#pragma unroll
+    for (int i = 0; i < RR; ++i)
+      if (ok[i]) acc[i] = fmaf(smem_rows[row[i] * per_row + in_off + k], wv, acc[i]);
+  }
+  const float bv = __ldg(b + col);
+#pragma unroll
+  for (int i = 0; i < RR; ++i)
+    if (ok[i]) smem_rows[row[i] * per_row + out_off + col] = acc[i] + bv;
+}
+
+// N: 2H for the transformer GEMVs, F for the attentive one.  Powers of two take
+// the compile-time mapping above (no predicates); other widths the general one.
+__device__ __forceinline__ void blk_gemv_n(float* sm, int per_row, int in_off, int out_off, int K,
+                                           const float* W, const float* b, int N) {
+  if (blk_gemv_pow2(sm, per_row, in_off, out_off, K, W, b, N)) return;
+  const int G = kBT / N;
+  const int rr = (kBR + G - 1) / G;
+  if (rr <= 1) blk_gemv_any<1>(sm, per_row, in_off, out_off, K, W, b, N);
+  else if (rr <= 2) blk_gemv_any<2>(sm, per_row, in_off, out_off, K, W, b, N);
+  else if (rr <= 4) blk_gemv_any<4>(sm, per_row, in_off, out_off, K, W, b, N);
+  else if (rr <= 8) blk_gemv_any<8>(sm, per_row, in_off, out_off, K, W, b, N);
+  else blk_gemv_any<16>(sm, per_row, in_off, out_off, K, W, b, N);
 }
 
 __device__ __forceinline__ void blk_glu(float* r, const BlkLayout& L, int H, bool residual, int lane) {
@@ -451,9 +514,9 @@ cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, 
   const int n2 = 2 * p.H;
   const int per_row_floats = 6 * rup4_host(p.F) + rup4_host(n2) + rup4_host(p.H) + rup4_host(p.ND);
   const size_t bsmem = (size_t)kBR * per_row_floats * sizeof(float);
-  const bool blk_ok = !per_row && (n2 == 32 || n2 == 64 || n2 == 128 || n2 == 256) &&
-                      (p.F == 32 || p.F == 64 || p.F == 128 || p.F == 256 || p.F == 512) &&
-                      p.ND % 4 == 0 && bsmem <= 227 * 1024;
+  // (F < 32, Adult: the per-row kernel measured slightly faster)
+  const bool blk_ok = !per_row && n2 <= kBT && p.F >= 32 && p.F <= kBT && p.ND % 4 == 0 &&
+                      bsmem <= 227 * 1024;
   if (blk_ok) {
     static bool bconf = false;
     if (!bconf) {

@@ -11,7 +11,7 @@ from paper_2510_19689_b200.network import TabNetModel
 
 tag = sys.argv[1]
 res = {}
-for cfg, rows in (("wide", 32768), ("bls", 65536), ("hr", 8192)):
+for cfg, rows in (("wide", 32768), ("bls", 65536), ("hr", 65536), ("adult", 4099)):
     m = TabNetModel.from_reference(W.make_model(cfg, "trained"), precision="fp32", device=0)
     r = DeviceRunner(m, rows, device=0)
     x = torch.from_numpy(W.make_inputs(W.WORKLOADS[cfg], rows)).cuda()

@@ -5,13 +5,18 @@
 #   then copy/summarize here with:  for f in gpurun_out/f_*.json ...; python tools/summarize_profiles.py
 set -e
 TAG=${TAG:-r1x}
+python tools/measure_tf32_peak.py > /dev/null     # -> gpurun_out/measured_tf32.json (copy into profiles/)
 python bench.py                                   > gpurun_out/f_hr_bf16.json
 python bench.py --precision tf32   --no-cpu-baseline > gpurun_out/f_hr_tf32.json
 python bench.py --precision tf32x3 --no-cpu-baseline > gpurun_out/f_hr_x3.json
 python bench.py --config adult                    > gpurun_out/f_adult_bf16.json
 python bench.py --config adult --precision tf32x3 --no-cpu-baseline > gpurun_out/f_adult_x3.json
 python bench.py --config bls                      > gpurun_out/f_bls_bf16.json
+python bench.py --config bls --precision tf32   --no-cpu-baseline > gpurun_out/f_bls_tf32.json
+python bench.py --config bls --precision tf32x3 --no-cpu-baseline > gpurun_out/f_bls_x3.json
+python bench.py --config bls --precision fp32   --no-cpu-baseline --steps 5 > gpurun_out/f_bls_fp32.json
 python bench.py --config hr_latency --rows 1024 --latency-sweep --no-cpu-baseline --steps 20 > gpurun_out/f_lat.json
 python bench.py --config wide --rows 262144 --steps 5 --warmup 3 > gpurun_out/f_wide_bf16.json
+python bench.py --config wide --precision fp32 --rows 262144 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/f_wide_fp32.json
 python bench.py --impl reference                  > gpurun_out/f_reference.json
 bash tools/profile.sh hr bf16 $TAG

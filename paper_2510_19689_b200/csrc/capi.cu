@@ -155,6 +155,9 @@ tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,
   if (device < 0 || device >= ndev) return fail(TBN_ERR_CONFIG, "device index out of range");
   if (precision != TBN_PREC_FP32 && !tbn::tc_supported(hp, precision))
     return fail(TBN_ERR_UNSUPPORTED, "no tcgen05 kernel instance for this model shape/precision");
+  if (precision == TBN_PREC_FP32 && !tbn::simt_supported(F, H, C))
+    return fail(TBN_ERR_UNSUPPORTED, "fp32 CUDA-core kernel supports feature_count <= 512, "
+                                     "2*(n_d+n_a) <= 256, n_classes <= 32");
 
   DeviceGuard guard(device);
   tbn_model* m = new tbn_model();
@@ -385,19 +388,64 @@ struct HostCtx {
 };
 constexpr size_t kMaxGraphs = 128;
 
+void free_host_ctx(int device, HostCtx* c) {
+  if (cudaSetDevice(device) != cudaSuccess) {   // runtime already torn down: nothing to free
+    cudaGetLastError();
+    return;
+  }
+  for (auto& sc : c->s)
+    if (sc.stream) cudaStreamSynchronize(sc.stream);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto& sc : c->s) {
+    if (sc.pin) cudaFreeHost(sc.pin);
+    if (sc.dev) cudaFree(sc.dev);
+    if (sc.stream) cudaStreamDestroy(sc.stream);
+  }
+  cudaGetLastError();
+  delete c;
+}
+
+// Per-thread owner of the host-path contexts: released when the thread exits
+// (the reference's invariance.py:40-41 spins up a fresh 32-thread pool per
+// call, so leaking them would grow pinned + device memory without bound).
+struct HostCtxOwner {
+  std::map<int, HostCtx*> ctxs;
+  ~HostCtxOwner() {
+    for (auto& kv : ctxs) free_host_ctx(kv.first, kv.second);
+  }
+};
+
 HostCtx* host_ctx(int device) {
   // Per-thread, per-device: apply() is reentrant and 32
   // concurrent callers (invariance.py:40-41) never share buffers or streams.
-  // Intentionally leaked at thread exit (CUDA may already be torn down).
-  thread_local std::map<int, HostCtx*> ctxs;
-  auto it = ctxs.find(device);
-  if (it != ctxs.end()) return it->second;
+  thread_local HostCtxOwner owner;
+  auto it = owner.ctxs.find(device);
+  if (it != owner.ctxs.end()) return it->second;
   HostCtx* c = new HostCtx();
   for (auto& sc : c->s)
-    if (cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-  ctxs[device] = c;
+    if (cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking) != cudaSuccess) {
+      free_host_ctx(device, c);
+      return nullptr;
+    }
+  owner.ctxs[device] = c;
   return c;
 }
+
+// On any early error return from the host path, wait for the chunks already
+// queued (their DMAs read/write the per-thread pinned staging) before the
+// next call may reuse that staging.
+struct DrainOnError {
+  HostCtx* hc;
+  bool armed = true;
+  ~DrainOnError() {
+    if (!armed) return;
+    for (auto& sc : hc->s) {
+      if (sc.stream) cudaStreamSynchronize(sc.stream);
+      sc.pending_r0 = -1;
+    }
+    cudaGetLastError();
+  }
+};
 
 cudaError_t ensure(StreamCtx* c, size_t pin_bytes, size_t dev_bytes) {
   if (c->pin_bytes < pin_bytes) {
@@ -523,9 +571,11 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     if (chunk < kMinChunk) chunk = kMinChunk;
   }
   const Layout L = layout_for(m, chunk, flags);
+  DrainOnError drain_guard{hc};
   for (auto& sc : hc->s) {
-    TBN_CUDA(ensure(&sc, direct ? 256 : L.total, L.total));
+    if (sc.pending_r0 >= 0) TBN_CUDA(cudaStreamSynchronize(sc.stream));   // (defensive: never left set)
     sc.pending_r0 = -1;
+    TBN_CUDA(ensure(&sc, direct ? 256 : L.total, L.total));
   }
   int32_t err_any = 0;
   const size_t err_off = direct ? 0 : L.err;   // pinned landing slot of the chunk's error flag
@@ -644,6 +694,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     tbn_status st = drain(sc);
     if (st != TBN_OK) return st;
   }
+  drain_guard.armed = false;
   if (err_any) return fail(TBN_ERR_INVALID_INPUT, "features must be finite");
   if (m->regression) {
     if (user.probabilities && user.probabilities != o.logits)

@@ -58,10 +58,12 @@ struct Cfg {
   static constexpr bool BF = (PREC == kPrecBF16);
   static constexpr int KG = BF ? 16 : 8;               // MMA K granule
   static constexpr int ESZ = BF ? 2 : 4;
-  // bias as an extra K row of B times a ones column of A at index F / H / NA
-  static constexpr int K1 = rup(F + 1, KG);
-  static constexpr int KHID = rup(H + 1, KG);
-  static constexpr int KATT = rup(NA + 1, KG);
+  // A operand = [1, 1, data..., stale]: the two ones (written once per tile)
+  // meet the bias hi/lo rows 0, 1 of every B block; data starts at element 2
+  static constexpr int A0 = 2;
+  static constexpr int K1 = rup(F + A0, KG);
+  static constexpr int KHID = rup(H + A0, KG);
+  static constexpr int KATT = rup(NA + A0, KG);
   static constexpr int FN = rup(F, 16);                // attentive N
   static constexpr int KA_EL = cmax(cmax(K1, KHID), KATT);
   static constexpr int KA = BF ? KA_EL / 2 : KA_EL;    // A operand TMEM columns
@@ -71,8 +73,11 @@ struct Cfg {
   static constexpr int NG_TMEM = 512 / TCG;
   // Register file: a row's live state is about 2F + H + 48 registers with xn
   // in registers (variant R), F + H + 48 with xn in shared memory (variant S).
-  static constexpr int NG_R = cmin(4, cmin(NG_TMEM, 65536 / (128 * (2 * F + H + 48))));
-  static constexpr int NG_S = cmin(4, cmin(NG_TMEM, 65536 / (128 * (F + H + 48))));
+#ifndef TBN_K2_MAXNG
+#define TBN_K2_MAXNG 4
+#endif
+  static constexpr int NG_R = cmin(TBN_K2_MAXNG, cmin(NG_TMEM, 65536 / (128 * (2 * F + H + 48))));
+  static constexpr int NG_S = cmin(TBN_K2_MAXNG, cmin(NG_TMEM, 65536 / (128 * (F + H + 48))));
   // weight blocks (B operands, N x K K-major canonical)
   static constexpr int PARTS = X3 ? 2 : 1;            // hi [+ lo] B blocks
   static constexpr int B_SH1 = PARTS * N2 * K1 * ESZ;
@@ -106,8 +111,19 @@ struct Cfg {
   static constexpr bool RING = IMG_BYTES + STG_ALL > SMEM_MAX;
   // 4 slots (measured: 8 buys nothing and takes L1 away)
   static constexpr int NSLOT_FIT = RING ? cmin(4, (SMEM_MAX - FIX_S - STG_ALL) / HBR) : 0;
-  static constexpr int NSLOT = NSLOT_FIT >= 8 ? 8 : NSLOT_FIT >= 4 ? 4 : NSLOT_FIT >= 2 ? 2 : 0;  // power of 2
+  static constexpr int NSLOT_SH = NSLOT_FIT >= 8 ? 8 : NSLOT_FIT >= 4 ? 4 : NSLOT_FIT >= 2 ? 2 : 0;  // power of 2
+  // per-group rings (GS slots each, no cross-group release protocol) when
+  // they fit: a shared ring ties every group to the slowest one
+#ifdef TBN_K2_GRING
+  static constexpr int GS_FIT = RING ? (SMEM_MAX - FIX_S - STG_ALL) / (NG * HBR) : 0;
+#else
+  static constexpr int GS_FIT = 0;
+#endif
+  static constexpr int GS = GS_FIT >= 3 ? 3 : GS_FIT;
+  static constexpr bool GRING = RING && GS >= 2;
+  static constexpr int NSLOT = GRING ? NG * GS : NSLOT_SH;   // slots in SMEM
   static_assert(!RING || NSLOT >= 2, "not even a 2-slot weight ring fits");
+  static_assert(NSLOT <= 16, "ring barriers");
   static constexpr int NB = 2 * (S + 1);               // ring blocks per tile: fc1_s, fc2_s
   static_assert(NG >= 1, "per-row state does not fit");
   static constexpr int TCOLS = pow2ceil(NG * TCG);
@@ -122,7 +138,8 @@ struct Cfg {
   static constexpr int OFF_STG = rup(RES_BYTES, 1024);
   static constexpr int OFF_XS = OFF_STG + NW * STG;    // variant S: per-warp xn tiles
   static constexpr int OFF_BAR = OFF_XS + (XS ? NW * STG : 0);
-  static constexpr int SMEM_BYTES = OFF_BAR + 512;
+  static constexpr int OFF_RCP = OFF_BAR + 512;        // rcp_rn(k), k = 0..F (sparsemax tau)
+  static constexpr int SMEM_BYTES = OFF_RCP + rup(4 * (F + 1), 128);
   static_assert(SMEM_BYTES <= 227 * 1024, "weights + staging exceed shared memory");
 };
 
@@ -135,8 +152,8 @@ struct Bars {
   uint64_t cfull;
   uint64_t dfull[4];       // per group: MMA chain complete
   uint64_t xfull[16];      // per warp: x row tile landed
-  uint64_t rfull[8];       // ring slots (variant S, streamed fc1/fc2 blocks)
-  uint32_t rcnt[8];        // ring slots: monotonic release counters
+  uint64_t rfull[16];      // ring slots (variant S, streamed fc1/fc2 blocks)
+  uint32_t rcnt[16];       // shared ring slots: monotonic release counters
   uint32_t tmem_base;
 };
 
@@ -171,14 +188,6 @@ __device__ __forceinline__ void put_a(uint32_t tA, const float (&v)[M]) {
     }
   }
 }
-// A elements [E, E+L) = ones at element E, zeros after (the bias column)
-template <class CF, int E, int L>
-__device__ __forceinline__ void put_ones(uint32_t tA) {
-  float v[L];
-#pragma unroll
-  for (int i = 0; i < L; ++i) v[i] = i == 0 ? 1.0f : 0.0f;
-  put_a<CF, E, L>(tA, v);
-}
 
 template <class CF>
 __global__ void __launch_bounds__(CF::THREADS, 1)
@@ -210,17 +219,30 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     const uint32_t i = v % NB;
     return p.wimg + ((i & 1) ? CF::O_FC2 : CF::O_FC1) + (i >> 1) * CF::HBR;
   };
+  // slot of block v: the CTA-wide ring, or this group's own GS slots (v is
+  // then the group's own block counter: its tiles are rounds 0, 1, ...)
+  auto ring_slot = [&](uint32_t v) -> int {
+    if constexpr (CF::GRING) return g * CF::GS + (int)(v % CF::GS);
+    else return (int)(v % NSLOT);
+  };
+  auto ring_parity = [&](uint32_t v) -> uint32_t {
+    if constexpr (CF::GRING) return (v / CF::GS) & 1u;
+    else return (v / NSLOT) & 1u;
+  };
   auto ring_load = [&](uint32_t v) {
-    const int sl = (int)(v % NSLOT);
+    const int sl = ring_slot(v);
     ptx::mbar_arrive_expect_tx(&bars->rfull[sl], CF::B_HID);
     ptx::bulk_g2s(smem + CF::OFF_RING + sl * CF::HBR, ring_src(v), CF::B_HID, &bars->rfull[sl]);
   };
+  // this group's tiles and ring blocks (per-group ring)
+  const int64_t rounds_g = tiles_cta > g ? (tiles_cta - g + NG - 1) / NG : 0;
+  const uint32_t nblk_g = (uint32_t)(rounds_g * NB);
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bars->cfull, 1);
     for (int i = 0; i < NG; ++i) ptx::mbar_init(&bars->dfull[i], 1);
     for (int i = 0; i < CF::NW; ++i) ptx::mbar_init(&bars->xfull[i], 1);
-    for (int i = 0; i < NSLOT; ++i) {
+    for (int i = 0; i < CF::NSLOT; ++i) {
       ptx::mbar_init(&bars->rfull[i], 1);
       bars->rcnt[i] = 0;
     }
@@ -240,13 +262,18 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       for (int o = 0; o < ATT_BYTES; o += CH)
         ptx::bulk_g2s(smem + CF::S_ATT + o, p.wimg + CF::O_ATT + o,
                       (uint32_t)(ATT_BYTES - o < CH ? ATT_BYTES - o : CH), &bars->cfull);
-      for (uint32_t v = 0; v < (uint32_t)NSLOT && v < nblk; ++v) ring_load(v);
+      if constexpr (!CF::GRING)
+        for (uint32_t v = 0; v < (uint32_t)NSLOT && v < nblk; ++v) ring_load(v);
     }
   }
   if (warp == 0) ptx::tmem_alloc<CF::TCOLS>(&bars->tmem_base);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  if constexpr (CF::GRING) {      // each group's issuing thread primes its own ring
+    if ((warp & 3) == 0 && lane == 0)
+      for (uint32_t v = 0; v < (uint32_t)CF::GS && v < nblk_g; ++v) ring_load(v);
+  }
   const uint32_t tg = bars->tmem_base + (uint32_t)(g * CF::TCG) + ((uint32_t)(q * 32) << 16);
   const uint32_t tD = tg + CF::T_D, tA = tg + CF::T_A, tPR = tg + CF::T_PR;
   float* stg = reinterpret_cast<float*>(smem + CF::OFF_STG + warp * CF::STG);
@@ -316,6 +343,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     const int nw0 = warp_rows(g, r0w);
     if (nw0 > 0) issue_x(r0w, nw0);
   }
+  float* const rcp_tab = reinterpret_cast<float*>(smem + CF::OFF_RCP);
+  for (int i = threadIdx.x; i <= F; i += blockDim.x) rcp_tab[i] = i ? __frcp_rn((float)i) : 0.0f;
   ptx::mbar_wait(&bars->cfull, 0);
   if (a.scale) {     // batch-statistics control: override the affine in this CTA's copy
     float* cw = reinterpret_cast<float*>(smem);
@@ -340,8 +369,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       // writing A (off the barrier -> MMA critical path)
       if (rv >= 0) {
         const uint32_t v = (uint32_t)rv;
-        if (q == 0) ptx::mbar_wait(&bars->rfull[v % NSLOT], (v / NSLOT) & 1u);
-        bo = CF::OFF_RING + (v % NSLOT) * CF::HBR;
+        if (q == 0) ptx::mbar_wait(&bars->rfull[ring_slot(v)], ring_parity(v));
+        bo = CF::OFF_RING + ring_slot(v) * CF::HBR;
       }
     }
     ptx::tmem_st_wait();
@@ -359,7 +388,12 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         // the previous GEMM's ring block: its MMAs completed before this chain
         // was issued, so release it now, off the critical path
         if (lane == 0 && ring_pending >= 0) {
-          ring_release((uint32_t)ring_pending);
+          if constexpr (CF::GRING) {
+            const uint32_t v = (uint32_t)ring_pending + CF::GS;
+            if (v < nblk_g) ring_load(v);
+          } else {
+            ring_release((uint32_t)ring_pending);
+          }
           ring_pending = -1;
         }
       }
@@ -385,17 +419,20 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   };
 
   // GLU block over D = [lin' | gate'] (H + H columns): gv <- lin'(1+t) [+ R gv]
-  auto glu = [&](bool residual) {
+  // for the output columns [CB, CE) (the whole block but where the reference's
+  // result is unused, Appendix A of SURVEY.md: step 0's d half, step S's a half)
+  auto glu_range = [&](bool residual, auto cb, auto ce) {
+    constexpr int CB = decltype(cb)::value, CE = decltype(ce)::value;
     constexpr int CW = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);   // 16 measured no faster
-    static_assert(H % CW == 0, "GLU chunking");
+    static_assert(H % CW == 0 && CB % CW == 0 && CE % CW == 0, "GLU chunking");
     float lin[CW], gate[CW];
-    tmem_load_n<CW>(tD, lin);
-    tmem_load_n<CW>(tD + H, gate);
+    tmem_load_n<CW>(tD + CB, lin);
+    tmem_load_n<CW>(tD + H + CB, gate);
     ptx::tmem_ld_wait();
 #pragma unroll
-    for (int c0 = 0; c0 < H; c0 += CW) {
+    for (int c0 = CB; c0 < CE; c0 += CW) {
       float ln2[CW], gt2[CW];
-      if (c0 + CW < H) {           // next chunk in flight while this one computes
+      if (c0 + CW < CE) {          // next chunk in flight while this one computes
         tmem_load_n<CW>(tD + c0 + CW, ln2);
         tmem_load_n<CW>(tD + H + c0 + CW, gt2);
       }
@@ -422,20 +459,21 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         gv[c0 + i] = o.x;
         gv[c0 + i + 1] = o.y;
       }
-      if (c0 + CW < H) {
+      if (c0 + CW < CE) {
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < CW; ++i) { lin[i] = ln2[i]; gate[i] = gt2[i]; }
       }
     }
   };
-  auto store_g = [&]() { put_a<CF, 0, H>(tA, gv); };
+  auto glu = [&](bool residual) { glu_range(residual, std::integral_constant<int, 0>{}, std::integral_constant<int, H>{}); };
+  auto store_g = [&]() { put_a<CF, CF::A0, H>(tA, gv); };
 
   for (int64_t k = 0; k < rounds; ++k) {
     const int64_t m = g + (int64_t)NG * k;
     if (m >= tiles_cta) {
       // no tile for this group in the last round: release its ring blocks
-      if constexpr (CF::RING) {
+      if constexpr (CF::RING && !CF::GRING) {
         if (tr) {
           if (ring_pending >= 0) ring_release((uint32_t)ring_pending);
           ring_pending = -1;
@@ -522,10 +560,12 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
 #pragma unroll
       for (int f = 0; f < F; ++f) one[f] = 1.0f;
       tmem_store_n<F>(tPR, one);
-      float av[CF::K1];
+      // the whole A row once per tile: the ones, xn, and zeros over every
+      // GEMM's padded K range (stale A elements must be finite: B rows are 0 there)
+      float av[CF::KA_EL];
 #pragma unroll
-      for (int e = 0; e < CF::K1; ++e) av[e] = e < F ? xv[e] : (e == F ? 1.0f : 0.0f);
-      put_a<CF, 0, CF::K1>(tA, av);
+      for (int e = 0; e < CF::KA_EL; ++e) av[e] = e < CF::A0 ? 1.0f : (e - CF::A0 < F ? xv[e - CF::A0] : 0.0f);
+      put_a<CF, 0, CF::KA_EL>(tA, av);
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) lacc[c] = 0.0f;
@@ -538,7 +578,6 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       gemm(0, CF::O_SH1, -1, post_first);
       glu(false);
       store_g();
-      put_ones<CF, H, CF::KHID - H>(tA);        // hidden-GEMM bias column
       gemm(1, CF::O_SH2, -1, nopost);
       glu(true);
       store_g();
@@ -546,7 +585,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       glu(true);
       store_g();
       gemm(1, o2, CF::RING ? rv0 + 2 * s + 1 : -1, nopost);
+#ifdef TBN_K2_PRUNE
+      if (s == 0) glu_range(true, std::integral_constant<int, ND>{}, std::integral_constant<int, H>{});
+      else if (s == S) glu_range(true, std::integral_constant<int, 0>{}, std::integral_constant<int, ND>{});
+      else glu(true);
+#else
       glu(true);
+#endif
     };
     // d = relu(f[:, :n_d]); eta = sum d; logits accumulate (the head is linear,
     // network.py:244, :253)
@@ -589,14 +634,14 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     transform(0, nopost);                                        // network.py:226-227
     float eta_prev = 0.0f;
     for (int s = 1; s <= S; ++s) {
-      // A <- [a = f[:, n_d:], 1, 0..]; under the attentive MMA: the previous
+      // A <- [1, 1, a = f[:, n_d:]]; under the attentive MMA: the previous
       // step's d/eta/logits and agg update
       {
-        float av[CF::KATT];
+        float av[NA];
 #pragma unroll
-        for (int e = 0; e < CF::KATT; ++e) av[e] = e < NA ? gv[ND + e] : (e == NA ? 1.0f : 0.0f);
+        for (int e = 0; e < NA; ++e) av[e] = gv[ND + e];
         if (s > 1) eta_prev = step_eta();
-        put_a<CF, 0, CF::KATT>(tA, av);
+        put_a<CF, CF::A0, NA>(tA, av);
       }
       gemm(2, CF::S_ATT + (uint32_t)(s - 1) * CF::ABR, -1, [&] {
         if (s > 1) agg_apply(eta_prev);
@@ -668,16 +713,18 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
           }
           if (cn >= cnt_prev) break;
           cnt_prev = cn;
-          tau = __fdividef(sm - 1.0f, cn);                            // sparsemax.py:39
+          // sparsemax.py:39: (sum - 1) / k as (sum - 1) * rcp_rn(k), k from the
+          // table (one rounding per operation: the emulation oracle repeats it)
+          tau = (sm - 1.0f) * rcp_tab[(int)cn];
         }
       }
-      // mask, prior update, x*mask -> A; mask -> staging (network.py:236-238, :246),
-      // in 16-feature chunks (A chunks of the shared1 K layout)
+      // mask, prior update, x*mask -> A (elements 2 ..); mask -> staging
+      // (network.py:236-238, :246), in 16-feature chunks
       if (tr) TBN_TRACE(g * 4000 + 3501 + 4 * s);
       claim_stg();
       {
         const float2 gm2 = f2(p.gamma, p.gamma), nt2 = f2(-tau, -tau);
-        chunked<CF::K1, 16>([&](auto o, auto l) {
+        chunked<(F + 1) / 2 * 2, 16>([&](auto o, auto l) {
           constexpr int O = decltype(o)::value, L = decltype(l)::value;
           constexpr int LF = (O + L <= F) ? L : (O < F ? F - O : 0);   // features in this chunk
           float pr[LF > 0 ? LF : 1], av[L];
@@ -707,13 +754,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
                   av[i + u] = mk * xn_at(fu);
                   my_stg[fu] = mk;
                 } else {
-                  av[i + u] = fu == F ? 1.0f : 0.0f;                      // ones column (bias row)
+                  av[i + u] = 0.0f;                                       // odd F: pad element
                 }
               }
             }
           }
           if constexpr (LF > 0) tmem_store_n<LF>(tPR + O, pr);
-          put_a<CF, O, L>(tA, av);
+          put_a<CF, O + CF::A0, L>(tA, av);
         });
       }
       // masks[s-1] of this warp's rows leave while the shared1 MMA runs
@@ -760,7 +807,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     }
     if (tr) TBN_TRACE(g * 4000 + 3003 + 8 * (int)k);
   }
-  if constexpr (CF::RING) {
+  if constexpr (CF::RING && !CF::GRING) {
     if (tr && ring_pending >= 0) ring_release((uint32_t)ring_pending);
   }
   if (lane == 0) ptx::bulk_wait0();

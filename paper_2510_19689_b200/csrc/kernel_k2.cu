@@ -48,19 +48,19 @@ bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
       cs_res[n] = n < H ? 0.5 * kR : 0.5;
     }
   }
-  using pack::pack_block;
+  using pack::pack_block_k2;
   constexpr int HB = tc::rup(CF::B_HID, 128);
-  pack_block(img, CF::O_SH1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first, hp.sh1_b, CF::BF);
-  pack_block(img, CF::O_SH2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, CF::X3, N2, &cs_res, hp.sh2_b, CF::BF);
+  pack_block_k2(img, CF::O_SH1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first, hp.sh1_b, CF::BF);
+  pack_block_k2(img, CF::O_SH2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, CF::X3, N2, &cs_res, hp.sh2_b, CF::BF);
   for (int s = 0; s <= S; ++s) {
-    pack_block(img, (CF::O_FC1 + s * HB) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
-               hp.fc1_b[s], CF::BF);
-    pack_block(img, (CF::O_FC2 + s * HB) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
-               hp.fc2_b[s], CF::BF);
+    pack_block_k2(img, (CF::O_FC1 + s * HB) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
+                  hp.fc1_b[s], CF::BF);
+    pack_block_k2(img, (CF::O_FC2 + s * HB) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
+                  hp.fc2_b[s], CF::BF);
   }
   for (int s = 1; s <= S; ++s)
-    pack_block(img, (CF::O_ATT + (s - 1) * tc::rup(CF::B_ATT, 128)) / 4, hp.att_W[s], NA, F, CF::FN, CF::KATT,
-               CF::X3, F, nullptr, hp.att_b[s], CF::BF);
+    pack_block_k2(img, (CF::O_ATT + (s - 1) * tc::rup(CF::B_ATT, 128)) / 4, hp.att_W[s], NA, F, CF::FN,
+                  CF::KATT, CF::X3, F, nullptr, hp.att_b[s], CF::BF);
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, CF::IMG_BYTES);
   if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), CF::IMG_BYTES, cudaMemcpyHostToDevice);
@@ -77,13 +77,8 @@ bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
 
 template <class CF>
 cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k2::tabnet_rowthread<CF>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = smem_attr_once<CF>((const void*)k2::tabnet_rowthread<CF>, CF::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
   // one CTA per SM, each with a contiguous, equal block of rows (k2_kernel.cuh);
   // small batches: one CTA per TBN_K2_ROWQ rows (spreading them thinner, 32
   // rows per CTA, measured no faster)
@@ -97,6 +92,14 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   K2Instance{F, ND, NA, S, C, P, &pack_k2<k2::Cfg<F, ND, NA, S, C, P>>,            \
              &launch_k2_impl<k2::Cfg<F, ND, NA, S, C, P>>}
 
+#ifdef TBN_K2_SINGLE   // dev A/B builds: one instance only, e.g. -DTBN_K2_SINGLE=K2_HR_BF16
+#define K2_HR_BF16 35, 16, 16, 5, 2, tc::kPrecBF16
+#define K2_HR_TF32 35, 16, 16, 5, 2, tc::kPrecTF32
+#define K2_HR_X3 35, 16, 16, 5, 2, tc::kPrecTF32x3
+#define K2_BLS_BF16 64, 32, 32, 5, 1, tc::kPrecBF16
+#define TBN_K2_EXPAND(...) TBN_K2(__VA_ARGS__)
+const K2Instance kK2[] = {TBN_K2_EXPAND(TBN_K2_SINGLE)};
+#else
 const K2Instance kK2[] = {
     TBN_K2(14, 8, 8, 3, 2, tc::kPrecTF32x3),   // Adult, 3xTF32 parity mode
     TBN_K2(35, 16, 16, 5, 2, tc::kPrecTF32x3), // HR, 3xTF32 parity mode
@@ -107,6 +110,7 @@ const K2Instance kK2[] = {
     TBN_K2(64, 32, 32, 5, 2, tc::kPrecBF16),   // BLS (its 2-class reference model)
     TBN_K2(64, 32, 32, 5, 1, tc::kPrecBF16),   // BLS regression head (TBN_CFG_REGRESSION)
 };
+#endif
 
 const K2Instance* find_k2(const HostParams& hp, int precision) {
   const int prec = precision == 0 ? tc::kPrecTF32x3 : precision == 1 ? tc::kPrecTF32

@@ -78,13 +78,8 @@ bool pack_k3(const HostParams& hp, TcModel* out, std::string* err) {
 
 template <class CF>
 cudaError_t launch_k3_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k3::tabnet_wide<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         CF::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = smem_attr_once<CF>((const void*)k3::tabnet_wide<CF>, CF::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
   if (!a.scratch) return cudaErrorInvalidValue;
   const int64_t ntiles = (a.rows + 127) / 128;
   int cap = num_sms;

@@ -501,14 +501,14 @@ size_t simt_smem_bytes(const SimtParams& p) {
   return (size_t)kWarpsPerBlock * (5 * p.F + 3 * p.H + p.ND + p.F) * sizeof(float);
 }
 
+bool simt_supported(int F, int H, int C) { return F <= kMaxF && 2 * H <= kMaxN && C <= 32; }
+
 cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
-  if (p.F > kMaxF || 2 * p.H > kMaxN || p.C > 32) return cudaErrorInvalidValue;
+  if (!simt_supported(p.F, p.H, p.C)) return cudaErrorInvalidValue;
   size_t smem = simt_smem_bytes(p);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tabnet_forward_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  struct SimtTag {};
+  cudaError_t ce = smem_attr_once<SimtTag>((const void*)tabnet_forward_simt, 200 * 1024);
+  if (ce != cudaSuccess) return ce;
   int64_t blocks_needed = (a.rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
   int64_t max_blocks = (int64_t)num_sms * 8;
   int grid = (int)(blocks_needed < max_blocks ? blocks_needed : max_blocks);
@@ -523,12 +523,11 @@ cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, 
   if (blk_ok) {
     const bool two = 2 * bsmem <= 227 * 1024;
     auto kern = two ? tabnet_forward_simt_blk<2> : tabnet_forward_simt_blk<1>;
-    static bool bconf = false;
-    if (!bconf) {
-      cudaFuncSetAttribute(tabnet_forward_simt_blk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      cudaFuncSetAttribute(tabnet_forward_simt_blk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      bconf = true;
-    }
+    struct Blk1Tag {};
+    struct Blk2Tag {};
+    ce = smem_attr_once<Blk1Tag>((const void*)tabnet_forward_simt_blk<1>, 227 * 1024);
+    if (ce == cudaSuccess) ce = smem_attr_once<Blk2Tag>((const void*)tabnet_forward_simt_blk<2>, 227 * 1024);
+    if (ce != cudaSuccess) return ce;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBT, bsmem);
     const int64_t nb = (a.rows + kBR - 1) / kBR;

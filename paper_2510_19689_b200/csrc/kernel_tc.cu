@@ -96,13 +96,9 @@ bool pack_impl(const HostParams& hp, TcModel* out, std::string* err) {
 
 template <class CF>
 cudaError_t launch_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
-  static bool configured = false;
   constexpr int smem = tc::Smem<CF>::TOTAL;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tc::tabnet_fused_tc<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = smem_attr_once<CF>((const void*)tc::tabnet_fused_tc<CF>, smem);
+  if (e != cudaSuccess) return e;
   const int64_t ntiles = (a.rows + 127) / 128;
   const int64_t npairs = (ntiles + CF::NG - 1) / CF::NG;
   const int grid = (int)(npairs < num_sms ? npairs : num_sms);

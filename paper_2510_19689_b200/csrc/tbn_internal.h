@@ -1,9 +1,29 @@
 // tbn_internal.h — internal (non-ABI) declarations of libtabnet_b200.
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace tbn {
+
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device): the
+// attribute is per CUDA context, and one process may drive several GPUs
+// (TabNetModel(device=N) caches one engine per device).  Thread-safe: the
+// public host API is reentrant.  `Tag` makes the state per kernel instance.
+constexpr int kMaxDevices = 64;
+template <class Tag>
+cudaError_t smem_attr_once(const void* func, int bytes) {
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t result[kMaxDevices];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [&] {
+    result[dev] = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  });
+  return result[dev];
+}
 
 // Pointers into the model's device buffer, fp32 row-major copies of the
 // reference params dict (network.py:81-96), used by the CUDA-core kernel.
@@ -37,6 +57,7 @@ struct ForwardArgs {
 };
 
 size_t simt_smem_bytes(const SimtParams& p);
+bool simt_supported(int F, int H, int C);      // the CUDA-core kernel's shape limits
 cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, cudaStream_t stream);
 cudaError_t launch_sparsemax(const float* z, int64_t rows, int n, float* out, int32_t* err_flag,
                              int num_sms, cudaStream_t stream);

@@ -209,12 +209,16 @@ class TabNetModel:
                 eng = self._engines.get(key)
                 if eng is None:
                     if prec == "auto":
+                        last = None
                         for cand in AUTO_ORDER:
                             try:
                                 eng = self._make_engine(cand, dev)
                                 break
-                            except UnsupportedShapeError:
-                                continue
+                            except UnsupportedShapeError as e:
+                                last = e
+                        if eng is None:
+                            raise UnsupportedShapeError(
+                                f"no kernel instance serves this model shape in any of {AUTO_ORDER}: {last}")
                     else:
                         eng = self._make_engine(prec, dev)
                     self._engines[key] = eng

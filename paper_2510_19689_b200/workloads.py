@@ -26,6 +26,7 @@ class Workload:
     batch: int
     description: str
     regression: bool = False     # evaluated through TabNetRegressor (identity head on column 0)
+    shard: bool = False          # bench default: the batch is row-sharded over the ranks (strong scaling)
 
     def model_config(self, seed: int = 0) -> ModelConfig:
         return ModelConfig(feature_count=self.feature_count, n_classes=self.n_classes,
@@ -43,11 +44,15 @@ WORKLOADS: dict[str, Workload] = {
                    "HR-attrition-shaped (35 features, n_d=n_a=16, n_steps=5) batch 65,536, with feature masks"),
     "bls": Workload("bls", 2, 64, 32, 32, 5, 2, 262144,
                     "BLS-shaped synthetic regression (64 features, n_d=n_a=32, n_steps=5) batch "
-                    "262,144, row-sharded", regression=True),
+                    "262,144, row-sharded", regression=True, shard=True),
     "hr_latency": Workload("hr_latency", 3, 35, 16, 16, 5, 2, 1024,
                            "HR shape latency sweep batch 1-1,024"),
     "wide": Workload("wide", 4, 512, 64, 64, 8, 10, 1 << 24,
-                     "wide TabNet (512 features, n_d=n_a=64, n_steps=8, 10 classes) 16M rows"),
+                     "wide TabNet (512 features, n_d=n_a=64, n_steps=8, 10 classes) 16M rows", shard=True),
+    # the north-star target: HR batch 65,536 row-sharded over the GPUs of one box
+    "hr8": Workload("hr8", 1, 35, 16, 16, 5, 2, 65536,
+                    "HR-attrition-shaped (35 features, n_d=n_a=16, n_steps=5) batch 65,536 row-sharded "
+                    "over the ranks (north star: 8xB200)", shard=True),
 }
 
 ATT_SCALE_TRAINED = 16.0   # SURVEY.md §8(d) "trained-like": step*_att_W x16
@@ -74,12 +79,28 @@ def make_norm_stats(w: Workload, seed: int = 7) -> tuple[np.ndarray, np.ndarray]
     return mean, var
 
 
+INPUT_BLOCK = 65536   # rows per independently seeded block of the input stream
+
+
 def make_inputs(w: Workload, rows: int, seed: int | None = None, start: int = 0) -> np.ndarray:
-    """float32 N(0,1) rows ``[start, start+rows)`` of the workload's stream."""
-    rng = np.random.default_rng(1000 + w.config_id if seed is None else seed)
-    if start:
-        rng.standard_normal((start, w.feature_count), dtype=np.float32)
-    return rng.standard_normal((rows, w.feature_count), dtype=np.float32)
+    """float32 N(0,1) rows ``[start, start+rows)`` of the workload's stream.
+
+    The stream is cut into blocks of ``INPUT_BLOCK`` rows, block b drawn from
+    its own generator (block 0 from ``default_rng(seed)``, so the first 65,536
+    rows are the plain ``default_rng(seed).standard_normal`` draw the golden
+    fixtures hold; block b > 0 from ``default_rng([seed, b])``).  A shard at a
+    large offset therefore costs only its own rows."""
+    base = 1000 + w.config_id if seed is None else seed
+    f = w.feature_count
+    out = np.empty((rows, f), dtype=np.float32)
+    if rows <= 0:
+        return out
+    for b in range(start // INPUT_BLOCK, (start + rows - 1) // INPUT_BLOCK + 1):
+        lo, hi = max(start, b * INPUT_BLOCK), min(start + rows, (b + 1) * INPUT_BLOCK)
+        rng = np.random.default_rng(base) if b == 0 else np.random.default_rng([base, b])
+        blk = rng.standard_normal((hi - b * INPUT_BLOCK, f), dtype=np.float32)   # prefix of the block
+        out[lo - start:hi - start] = blk[lo - b * INPUT_BLOCK:]
+    return out
 
 
 def make_engine_model(name: str, regime: str = "trained", *, precision: str = "auto",

@@ -75,3 +75,64 @@ def test_l2_plan_rotates_past_l2_or_flushes(bench):
         else:
             assert nsets * per_set >= 2 * bench.L2_BYTES      # every step streams from HBM
         assert flush == (name in ("adult", "hr_latency"))
+
+
+def test_rank_row_plans(bench):
+    """Weak scaling gives every rank its own full batch; --shard (default for BLS,
+    wide and hr8) splits the config's batch into contiguous shards."""
+    a = bench.parse(["--config", "bls"])
+    w = W.WORKLOADS["bls"]
+    plans = [bench.plan_rows(w, a, r, 4) for r in range(4)]
+    assert [p[0] for p in plans] == [65536] * 4 and [p[1] for p in plans] == [0, 65536, 131072, 196608]
+    assert all(p[2] for p in plans)
+    a = bench.parse(["--config", "hr"])
+    rows, start, sh = bench.plan_rows(W.WORKLOADS["hr"], a, 3, 8)
+    assert (rows, start, sh) == (65536, 3 * 65536, False)
+    a = bench.parse(["--config", "hr8"])
+    assert bench.plan_rows(W.WORKLOADS["hr8"], a, 7, 8) == (8192, 7 * 8192, True)
+    a = bench.parse(["--config", "bls", "--no-shard"])
+    assert bench.plan_rows(w, a, 1, 2) == (262144, 262144, False)
+    a = bench.parse(["--config", "hr8", "--rows", "1000"])          # explicit rows: weak
+    assert bench.plan_rows(W.WORKLOADS["hr8"], a, 1, 2) == (1000, 1000, False)
+
+
+def test_both_arms_print_the_same_config(bench):
+    for cfg in ("hr", "bls", "hr8"):
+        a = bench.parse(["--config", cfg])
+        w = W.WORKLOADS[cfg]
+        rows, _, sh = bench.plan_rows(w, a, 0, 2)
+        c = bench.bench_config(w, a, rows, 2, sh)
+        assert c == bench.bench_config(w, bench.parse(["--config", cfg, "--impl", "reference"]), rows, 2, sh)
+        assert "precision" not in c and c["rows_per_rank"] == rows
+
+
+def test_chunked_stream_plan(bench):
+    bpr = W.algorithmic_counts(W.WORKLOADS["wide"])["bytes_per_row"]
+    ch, n = bench.chunk_plan(1 << 24, bpr)
+    assert ch % 128 == 0 and ch * bpr <= bench.MAX_CHUNK_BYTES and ch * n >= 1 << 24 and ch * (n - 1) < 1 << 24
+    assert bench.chunk_plan(65536, 1000) == (65536, 1)
+
+
+def test_self_launch_command(bench):
+    cmd = bench.launch_cmd(4, ["--config", "bls"], 29999)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1" and cmd[-2:] == ["--config", "bls"]
+
+
+def test_two_rank_launch_and_reduction_gloo():
+    """`bench.py --gpus 2` with WORLD_SIZE unset re-launches itself under
+    torch.distributed.run (2 ranks, gloo for --dry-run): rank 0 prints n_gpus 2,
+    the shard plan, the max of the per-rank times and the sum of their rows."""
+    import os
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "bls", "--dry-run"],
+                       capture_output=True, text=True, timeout=240, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["rows_per_rank"] == 131072 and d["rows_all_ranks"] == 262144
+    assert d["max_ms"] == 2.0 and d["shards"] == [[0, 131072], [131072, 131072]]
+    assert d["scaling"] == "strong"

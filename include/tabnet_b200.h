@@ -27,14 +27,19 @@
 extern "C" {
 #endif
 
-#define TBN_ABI_VERSION 1
+#define TBN_ABI_VERSION 2
 
 typedef enum {
   TBN_OK = 0,
   TBN_ERR_INVALID_INPUT = 1, /* width mismatch, non-finite feature, rows < 1   (network.py:207-211) */
   TBN_ERR_CONFIG = 2,        /* inconsistent config / params                   (config.py:29-41, network.py:110-114) */
   TBN_ERR_CUDA = 3,          /* CUDA runtime failure or no device                                         */
-  TBN_ERR_UNSUPPORTED = 4    /* shape outside the compiled kernel instances                               */
+  TBN_ERR_UNSUPPORTED = 4,   /* shape outside the compiled kernel instances                               */
+  /* .tbnt stream errors, the ModelFormatError family of io.py:60-112 / errors.py:20-33 */
+  TBN_ERR_FORMAT = 5,        /* ModelFormatError: bad magic, trailing bytes, metadata, size mismatch   */
+  TBN_ERR_FORMAT_VERSION = 6,/* FormatVersionError: version != 1                                       */
+  TBN_ERR_TRUNCATED = 7,     /* TruncatedStreamError: stream ends inside the header or a section        */
+  TBN_ERR_CHECKSUM = 8       /* ChecksumError: CRC-32C trailer mismatch                                  */
 } tbn_status;
 
 /* Arithmetic of the FC contractions.  Everything else (GLU, sparsemax, prior,
@@ -95,6 +100,10 @@ typedef struct tbn_model tbn_model;
 int32_t tbn_abi_version(void);
 const char* tbn_last_error(void);                   /* thread-local, never NULL */
 int32_t tbn_device_count(void);                     /* 0 when no CUDA device is usable */
+/* Create the device's primary CUDA context now (a server's warm-up; the
+ * cold-start split of tools/cold_start.py).  Optional: every call creates it
+ * on first use. */
+tbn_status tbn_device_init(int32_t device);
 
 /* Build a device-resident model from the reference's params dict
  * (network.py:71-97 names and shapes, row-major float64, used as x @ W) and
@@ -152,6 +161,54 @@ tbn_status tbn_partition_mean(const float* values, int64_t rows_per_partition, i
 /* CRC-32C (Castagnoli, reflected 0x82F63B78) as io.py:22-36, hardware
  * accelerated on the host CPU when SSE4.2 is present.  Pure host code. */
 uint32_t tbn_crc32c(const uint8_t* data, size_t n, uint32_t crc);
+
+/* ---- .tbnt model streams (io.py:43-112; pure host code) ----------------
+ * tbn_tbnt_parse replaces load_model (io.py:60-112): header, sections, CRC,
+ * metadata JSON, ModelConfig / TabNetModel invariants, in the reference's
+ * order and error classes (TBN_ERR_TRUNCATED / FORMAT / FORMAT_VERSION /
+ * CHECKSUM / CONFIG).  The handle owns float64 copies of every parameter in
+ * param_order and of the normalization stats. */
+typedef struct tbn_tbnt tbn_tbnt;
+tbn_status tbn_tbnt_parse(const uint8_t* data, size_t n, tbn_tbnt** out);
+void tbn_tbnt_free(tbn_tbnt* t);
+/* ModelConfig fields (lambda_sparse, seed beside tbn_config), model_version, #params */
+tbn_status tbn_tbnt_info(const tbn_tbnt* t, tbn_config* cfg, double* lambda_sparse, int64_t* seed,
+                         const char** model_version, int32_t* n_params);
+/* parameter i of param_order: name, ndim, dims (<= 8), row-major float64 data */
+tbn_status tbn_tbnt_param(const tbn_tbnt* t, int32_t i, const char** name, int32_t* ndim,
+                          int64_t* dims, const double** data);
+tbn_status tbn_tbnt_norm(const tbn_tbnt* t, const double** mean, const double** var);
+/* The cold-start path: parse + verify the stream and build the device model
+ * (weights packed for `precision` and uploaded to `device`) in one call, no
+ * Python-side parsing.  cfg_flags = TBN_CFG_REGRESSION serves head column
+ * `head_column` of the stored classifier as an identity head (TabNetRegressor). */
+tbn_status tbn_model_create_from_tbnt(const uint8_t* data, size_t n, int32_t precision, int32_t device,
+                                      int32_t cfg_flags, int32_t head_column, tbn_model** out);
+
+/* ---- device preprocessing (data/preprocess.py:68-122, the numeric tail) ----
+ * The host maps each raw cell to one float64 code (the string -> level lookup
+ * stays on the host): standardize/passthrough -> the value or NaN if missing,
+ * ordinal -> the plan's level integer or -1, onehot -> the category index or -1.
+ * tbn_preprocess expands (rows x ncols) device codes into the model's float32
+ * input (rows x width): median imputation, (v - mean) / std in float64 rounded
+ * once (= the reference's float64 matrix cast to float32), ordinal values,
+ * one-hot blocks of `width` levels, columns in plan order. */
+#define TBN_PREP_STANDARDIZE 0
+#define TBN_PREP_PASSTHROUGH 1
+#define TBN_PREP_ORDINAL 2
+#define TBN_PREP_ONEHOT 3
+typedef struct {
+  int32_t kind;     /* TBN_PREP_*                                  */
+  int32_t width;    /* one-hot: number of categories; else 1       */
+  double median;    /* imputation value (standardize, passthrough) */
+  double mean;      /* standardize                                 */
+  double std;       /* standardize (ddof=1, never 0)               */
+} tbn_prep_column;
+typedef struct tbn_prep tbn_prep;
+tbn_status tbn_prep_create(const tbn_prep_column* cols, int32_t ncols, int32_t device, tbn_prep** out);
+void tbn_prep_destroy(tbn_prep* plan);
+int32_t tbn_prep_width(const tbn_prep* plan);
+tbn_status tbn_preprocess(const tbn_prep* plan, const double* codes, int64_t rows, float* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -12,12 +12,15 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import (ConfigurationError, DeviceError, InvalidInputError, TabserveError,
+from .errors import (ChecksumError, ConfigurationError, DeviceError, FormatVersionError,
+                     InvalidInputError, ModelFormatError, TabserveError, TruncatedStreamError,
                      UnsupportedShapeError)
 
 LIB_PATH = Path(__file__).resolve().parent / "libtabnet_b200.so"
 
-TBN_OK, TBN_ERR_INVALID_INPUT, TBN_ERR_CONFIG, TBN_ERR_CUDA, TBN_ERR_UNSUPPORTED = range(5)
+(TBN_OK, TBN_ERR_INVALID_INPUT, TBN_ERR_CONFIG, TBN_ERR_CUDA, TBN_ERR_UNSUPPORTED, TBN_ERR_FORMAT,
+ TBN_ERR_FORMAT_VERSION, TBN_ERR_TRUNCATED, TBN_ERR_CHECKSUM) = range(9)
+ABI_VERSION = 2
 PREC_TF32X3, PREC_TF32, PREC_BF16, PREC_FP32 = range(4)
 CFG_REGRESSION = 1           # tbn_config.flags: identity head, n_classes == 1
 PRECISIONS = {"tf32x3": PREC_TF32X3, "tf32": PREC_TF32, "bf16": PREC_BF16, "fp32": PREC_FP32}
@@ -26,10 +29,13 @@ FLAG_BATCH_STATS = 2
 
 # Every symbol include/tabnet_b200.h declares (tests check the .so exports them).
 EXPORTED = (
-    "tbn_abi_version", "tbn_last_error", "tbn_device_count", "tbn_model_create",
+    "tbn_abi_version", "tbn_last_error", "tbn_device_count", "tbn_device_init", "tbn_model_create",
     "tbn_model_destroy", "tbn_model_info", "tbn_workspace_bytes", "tbn_forward",
     "tbn_forward_host", "tbn_forward_host_f64", "tbn_sparsemax",
     "tbn_sparsemax_host_f64", "tbn_partition_mean", "tbn_crc32c",
+    "tbn_tbnt_parse", "tbn_tbnt_free", "tbn_tbnt_info", "tbn_tbnt_param", "tbn_tbnt_norm",
+    "tbn_model_create_from_tbnt", "tbn_prep_create", "tbn_prep_destroy", "tbn_prep_width",
+    "tbn_preprocess",
 )
 
 
@@ -37,6 +43,11 @@ class TbnConfig(C.Structure):
     _fields_ = [("feature_count", C.c_int32), ("n_classes", C.c_int32), ("n_d", C.c_int32),
                 ("n_a", C.c_int32), ("n_steps", C.c_int32), ("flags", C.c_int32),
                 ("gamma", C.c_double)]
+
+
+class TbnPrepColumn(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("width", C.c_int32), ("median", C.c_double), ("mean", C.c_double),
+                ("std", C.c_double)]
 
 
 class TbnOutputs(C.Structure):
@@ -66,6 +77,8 @@ def lib() -> C.CDLL:
         L.tbn_abi_version.restype = i32
         L.tbn_last_error.restype = C.c_char_p
         L.tbn_device_count.restype = i32
+        L.tbn_device_init.restype = i32
+        L.tbn_device_init.argtypes = [i32]
         L.tbn_model_create.restype = i32
         L.tbn_model_create.argtypes = [C.POINTER(TbnConfig), C.POINTER(C.c_char_p),
                                        C.POINTER(C.c_void_p), C.POINTER(C.c_int64), i32,
@@ -90,7 +103,29 @@ def lib() -> C.CDLL:
         L.tbn_sparsemax_host_f64.argtypes = [vp, i64, i32, vp]
         L.tbn_crc32c.restype = u32
         L.tbn_crc32c.argtypes = [C.c_char_p, sz, u32]
-        if L.tbn_abi_version() != 1:
+        L.tbn_tbnt_parse.restype = i32
+        L.tbn_tbnt_parse.argtypes = [C.c_char_p, sz, C.POINTER(vp)]
+        L.tbn_tbnt_free.restype = None
+        L.tbn_tbnt_free.argtypes = [vp]
+        L.tbn_tbnt_info.restype = i32
+        L.tbn_tbnt_info.argtypes = [vp, C.POINTER(TbnConfig), C.POINTER(C.c_double), C.POINTER(i64),
+                                    C.POINTER(C.c_char_p), C.POINTER(i32)]
+        L.tbn_tbnt_param.restype = i32
+        L.tbn_tbnt_param.argtypes = [vp, i32, C.POINTER(C.c_char_p), C.POINTER(i32), C.POINTER(i64),
+                                     C.POINTER(C.POINTER(C.c_double))]
+        L.tbn_tbnt_norm.restype = i32
+        L.tbn_tbnt_norm.argtypes = [vp, C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.POINTER(C.c_double))]
+        L.tbn_model_create_from_tbnt.restype = i32
+        L.tbn_model_create_from_tbnt.argtypes = [C.c_char_p, sz, i32, i32, i32, i32, C.POINTER(vp)]
+        L.tbn_prep_create.restype = i32
+        L.tbn_prep_create.argtypes = [C.POINTER(TbnPrepColumn), i32, i32, C.POINTER(vp)]
+        L.tbn_prep_destroy.restype = None
+        L.tbn_prep_destroy.argtypes = [vp]
+        L.tbn_prep_width.restype = i32
+        L.tbn_prep_width.argtypes = [vp]
+        L.tbn_preprocess.restype = i32
+        L.tbn_preprocess.argtypes = [vp, vp, i64, vp, vp]
+        if L.tbn_abi_version() != ABI_VERSION:
             raise DeviceError("libtabnet_b200.so ABI version mismatch")
         _lib = L
         return _lib
@@ -113,6 +148,14 @@ def check(status: int, what: str = "") -> None:
         raise UnsupportedShapeError(msg)
     if status == TBN_ERR_CUDA:
         raise DeviceError(msg)
+    if status == TBN_ERR_FORMAT:
+        raise ModelFormatError(msg)
+    if status == TBN_ERR_FORMAT_VERSION:
+        raise FormatVersionError(msg)
+    if status == TBN_ERR_TRUNCATED:
+        raise TruncatedStreamError(msg)
+    if status == TBN_ERR_CHECKSUM:
+        raise ChecksumError(msg)
     raise TabserveError(f"status {status}: {msg}")
 
 

@@ -32,7 +32,8 @@ if os.environ.get("TBN_TRACE_BUILD"):          # development timeline build (see
 if os.environ.get("TBN_EXTRA_FLAGS"):          # development A/B variants (tools/ab.sh)
     CU_FLAGS += os.environ["TBN_EXTRA_FLAGS"].split()
 CXX = shutil.which("g++") or "g++"
-CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+CUDA_INC = Path(NVCC).resolve().parent.parent / "include"
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{CUDA_INC}"]
 
 
 def sources() -> list[Path]:

@@ -57,6 +57,8 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
+void tbn::set_last_error(const std::string& msg) { g_last_error = msg; }
+
 struct tbn_model {
   uint64_t id = 0;             // unique per created model (keys the host path's graph cache)
   tbn_config cfg{};
@@ -81,6 +83,15 @@ int32_t tbn_device_count(void) {
     return 0;
   }
   return n;
+}
+
+tbn_status tbn_device_init(int32_t device) {
+  if (device < 0 || device >= tbn_device_count()) return fail(TBN_ERR_CUDA, "no such CUDA device");
+  DeviceGuard guard(device);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaFree(nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "context init");
+  return TBN_OK;
 }
 
 tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,

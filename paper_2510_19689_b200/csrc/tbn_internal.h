@@ -2,9 +2,12 @@
 #pragma once
 #include <cstdint>
 #include <mutex>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace tbn {
+
+void set_last_error(const std::string& msg);   // tbn_last_error() of this thread
 
 // Raise a kernel's dynamic shared-memory limit once per (kernel, device): the
 // attribute is per CUDA context, and one process may drive several GPUs

@@ -120,6 +120,31 @@ class DeviceModel:
         self.device = device
         self._lib = L
 
+    @classmethod
+    def from_tbnt(cls, stream: bytes, precision: str, device: int, *, regression: bool = False,
+                  head_column: int = 0) -> "DeviceModel":
+        """The cold-start path: a .tbnt stream (reference io.py:43-57) parsed,
+        CRC-checked, packed and uploaded by one native call."""
+        L = N.lib()
+        if precision not in N.PRECISIONS:
+            raise ConfigurationError(f"unknown precision {precision!r}; one of {sorted(N.PRECISIONS)}")
+        handle = C.c_void_p()
+        N.check(L.tbn_model_create_from_tbnt(stream, len(stream), N.PRECISIONS[precision], int(device),
+                                             N.CFG_REGRESSION if regression else 0, int(head_column),
+                                             C.byref(handle)), "tbn_model_create_from_tbnt")
+        self = cls.__new__(cls)
+        cfg = N.TbnConfig()
+        prec, dev = C.c_int32(), C.c_int32()
+        N.check(L.tbn_model_info(handle, C.byref(cfg), C.byref(prec), C.byref(dev)))
+        self.handle = handle
+        self.n_out = cfg.n_classes
+        self.config = ModelConfig(feature_count=cfg.feature_count, n_classes=max(2, cfg.n_classes),
+                                  n_d=cfg.n_d, n_a=cfg.n_a, n_steps=cfg.n_steps, gamma=cfg.gamma)
+        self.precision = precision
+        self.device = device
+        self._lib = L
+        return self
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:

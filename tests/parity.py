@@ -1,7 +1,8 @@
 """Tie-aware parity comparator shared by the GPU tests.
 
 A row is EXEMPT when the float64 reference's own sparsemax margin at any step,
-min_i |z_i - tau| / max|z|, is below ``delta`` (the support set there is decided
+min_i |z_i - tau| / max|z|, is below ``delta`` (default 2e-5; every fp32 / 3xTF32
+support flip measured on B200 had a margin below 2.7e-6) (the support set there is decided
 by rounding, not by the model), or — for the class check only — when its top-2
 probability gap is below ``gap``.  On every other row: identical sparsemax
 support sets at every step, identical predicted class, and values within
@@ -43,7 +44,7 @@ class ParityReport:
                 f"max_err={ {k: float(f'{v:.3g}') for k, v in self.max_err.items()} } viol={self.viol}")
 
 
-def compare(ref: dict, got: dict, *, delta: float = 1e-4, gap: float = 1e-6,
+def compare(ref: dict, got: dict, *, delta: float = 2e-5, gap: float = 1e-6,
             rtol: float = 1e-4, atol: dict | None = None) -> ParityReport:
     atol = {"logits": 1e-6, "probabilities": 1e-6, "masks": 1e-6, "importance": 1e-6,
             **(atol or {})}

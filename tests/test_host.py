@@ -36,7 +36,7 @@ def test_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(N.LIB_PATH))
     for sym in declared:
         assert hasattr(lib, sym), sym
-    assert N.lib().tbn_abi_version() == 1
+    assert N.lib().tbn_abi_version() == N.ABI_VERSION == 2
 
 
 def test_crc32c_native_matches_reference_table():
@@ -179,3 +179,27 @@ def test_from_reference_duck_typing():
     m2 = P.TabNetModel.from_reference(m, precision="fp32")
     assert m2.precision == "fp32" and m2.config == m.config
     assert all(np.array_equal(m.params[k], m2.params[k]) for k in m.params)
+
+
+def test_native_tbnt_reader_replays_reference_cases():
+    """csrc/tbnt.cpp against the unmodified reference loader (io.py:60-112) on
+    the malformed and unusual streams of tests/golden/make_tbnt_cases.py: the same
+    exception class for every rejected stream, the same model (re-serialized
+    bytes) for every accepted one."""
+    g = np.load(GOLDEN / "tbnt_cases.npz")
+    names = sorted({k.split("__")[0] for k in g.files})
+    assert len(names) >= 20
+    classes = {"ok": None, "TruncatedStreamError": P.TruncatedStreamError,
+               "ModelFormatError": P.ModelFormatError, "FormatVersionError": P.FormatVersionError,
+               "ChecksumError": P.ChecksumError, "ConfigurationError": P.ConfigurationError}
+    for name in names:
+        stream = g[name + "__stream"].tobytes()
+        expect = str(g[name + "__expect"])
+        if expect == "ok":
+            m = P.load_model(stream)
+            assert P.save_model(m) == g[name + "__reserialized"].tobytes(), name
+        else:
+            with pytest.raises(classes[expect]) as ei:
+                P.load_model(stream)
+            # the exact class, not a sibling of the ModelFormatError family
+            assert type(ei.value) is classes[expect], (name, type(ei.value))

@@ -1,8 +1,11 @@
 """GPU parity: the CUDA path against the reference-pinned oracle/goldens.
 
 Tie-aware rule (parity.py): on every row whose reference
-sparsemax margin is >= 1e-4 at all steps, identical support sets and class and
-values within 1e-4 relative (+1e-6 absolute).  Exempt rows are counted.
+sparsemax margin is >= 2e-5 (1e-5 for HR @ 65,536) at all steps, identical
+support sets and class and values within 1e-4 relative (+1e-6 absolute).
+Exempt rows are counted.  The single-pass modes (bf16, tf32) are held tightly
+against the rounding-faithful emulation (oracle/tabnet_emulate.py) and loosely
+against the float64 oracle.
 """
 import threading
 
@@ -75,10 +78,12 @@ def test_full_size_hr_against_oracle(precision):
     p = np.sort(ref["probabilities"], axis=1)
     ref["top2_gap"] = p[:, -1] - p[:, -2]
     r = m.apply(x)
-    rep = compare(ref, _res_dict(r))
+    rep = compare(ref, _res_dict(r), delta=1e-5)
     print("hr65536", precision, rep.summary())
     assert rep.ok, rep.summary()
-    assert len(rep.exempt_rows) < 65536 // 10
+    # measured: 291 exempt rows (0.44%); every support flip of the fp32 / 3xTF32
+    # kernels sits at a reference margin below 2.7e-6
+    assert len(rep.exempt_rows) < 65536 // 200
     # size-independent properties on all rows
     np.testing.assert_allclose(r.masks.sum(axis=2), 1.0, atol=1e-5)
     assert np.all(r.masks >= 0)
@@ -433,9 +438,8 @@ def test_sampled_parity_at_full_size(name, precision):
         ref["margin"] = np.abs(zs - tau[..., None]).min(axis=2) / np.maximum(np.abs(zs).max(axis=2), 1e-300)
         rep = compare(ref, got)
         assert rep.ok, rep.summary()
-        # near-ties (margin < 1e-4) are common at F = 512 (194 of 512 sampled rows
-        # remain compared for wide); they must not swallow the check
-        assert len(idx) - len(rep.exempt_rows) >= (len(idx) // 2 if name != "wide" else 128)
+        # near-ties are common at F = 512; they must not swallow the check
+        assert len(idx) - len(rep.exempt_rows) >= (len(idx) * 9 // 10 if name != "wide" else len(idx) // 2)
     else:
         ref["margin"] = np.ones((m.config.n_steps, len(idx)))
         rep = compare(ref, got, delta=0.0, gap=5e-2, rtol=2.5e-1, atol={"probabilities": 3e-2, "logits": 2e-1})
@@ -498,3 +502,76 @@ def test_host_call_pinned_buffers_graph_replay(precision):
         xp[rows // 2, 3] = float("nan")
         with pytest.raises(P.InvalidInputError):
             eng.forward_host_f32(xp.numpy(), 0, npo)
+
+
+def _emu_stats(got, emu):
+    mass = np.abs(emu["masks"]).sum(-1)
+    me = np.abs(np.asarray(got["masks"]) - emu["masks"]).max(-1) / np.maximum(mass, 1e-30)
+    return dict(mask_max=float(me.max()), mask_p999=float(np.quantile(me, 0.999)),
+                mask_p99=float(np.quantile(me, 0.99)),
+                imp_max=float(np.abs(np.asarray(got["importance"]) - emu["importance"]).max()),
+                prob_max=float(np.abs(np.asarray(got["probabilities"]) - emu["probabilities"]).max()))
+
+
+# (mask max, mask p99.9, importance max, probability max) against the emulation;
+# measured on B200 (HR @ 65,536, trained-like weights): bf16 2.5e-2 / 3.5e-3 /
+# 1.3e-2 / 1.6e-3, tf32 1.1e-2 / 1.1e-3 / 4.8e-3 / 8.9e-4 — against the float64
+# oracle the same kernel is at 0.21 / 4.3e-2 / 6.0e-2 / 2.0e-2 (bf16).
+EMU_BOUNDS = {"bf16": (5e-2, 7e-3, 2.5e-2, 4e-3), "tf32": (2.5e-2, 2.5e-3, 1e-2, 2e-3)}
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+@pytest.mark.parametrize("name,rows,bias", [("hr", 65536, False), ("hr", 65536, True), ("adult", 4096, True),
+                                            ("bls", 16384, False)])
+def test_single_pass_modes_against_emulation(precision, name, rows, bias):
+    """The single-pass modes against oracle/tabnet_emulate.py, which repeats the
+    K2 kernel's operand rounding (bf16 RNE / tf32), folded GLU constants, bias
+    hi/lo rows and float32 epilogue order; what remains is the tanh.approx
+    error and the tensor core's summation order.  All rows, every output, plus
+    identical classes wherever the emulation's top-2 gap is >= 1e-3."""
+    from oracle import tabnet_emulate as E
+    w = W.WORKLOADS[name]
+    base = W.make_model(name, "trained")
+    params = base.params
+    if bias:
+        rng = np.random.default_rng(11)
+        params = {k: (v + rng.normal(0.0, 0.3, v.shape) if k.endswith("_b") else v) for k, v in params.items()}
+    m = P.TabNetModel(config=base.config, params=params, norm_mean=base.norm_mean, norm_var=base.norm_var,
+                      model_version="emu", precision=precision)
+    x = W.make_inputs(w, rows)
+    r = m.apply(x.astype(np.float64))
+    emu = E.apply_model_emulated(m, x, mode=precision)
+    st = _emu_stats(_res_dict(r), emu)
+    print(name, rows, precision, "bias" if bias else "", st)
+    mmax, mp999, imax, pmax = EMU_BOUNDS[precision]
+    assert st["mask_max"] < mmax and st["mask_p999"] < mp999, st
+    assert st["imp_max"] < imax and st["prob_max"] < pmax, st
+    p = np.sort(emu["probabilities"], axis=1)
+    sure = (p[:, -1] - p[:, -2]) >= 1e-3
+    assert np.array_equal(np.argmax(r.probabilities, 1)[sure], np.argmax(emu["probabilities"], 1)[sure])
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32x3"])
+def test_device_model_from_tbnt_stream(precision):
+    """The cold-start path (tbn_model_create_from_tbnt: the C++ parser feeds the
+    packer directly) serves bitwise the same outputs as the engine built from
+    the params dict; the regression variant takes head column 0."""
+    from paper_2510_19689_b200 import io as PIO
+    m = P.TabNetModel.from_reference(W.make_model("hr"), precision=precision)
+    stream = P.save_model(m)
+    eng = PIO.load_device_model(stream, precision=precision, device=0)
+    x = W.make_inputs(W.WORKLOADS["hr"], 777).astype(np.float64)
+    a = eng.forward_host_f64(x, 0)
+    b = m.engine().forward_host_f64(x, 0)
+    for k in ("logits", "probabilities", "masks", "importance", "predicted_class"):
+        assert np.array_equal(a[k], b[k]), k
+    from paper_2510_19689_b200.network import DeviceModel
+    bls = W.make_model("bls")
+    reg = DeviceModel.from_tbnt(P.save_model(bls), precision, 0, regression=True, head_column=0)
+    want = P.TabNetRegressor.from_reference(bls, head_column=0, precision=precision)
+    xb = W.make_inputs(W.WORKLOADS["bls"], 300).astype(np.float64)
+    assert np.array_equal(reg.forward_host_f64(xb, 0)["logits"], want.engine().forward_host_f64(xb, 0)["logits"])
+    bad = bytearray(stream)
+    bad[50] ^= 1
+    with pytest.raises(P.ChecksumError):
+        PIO.load_device_model(bytes(bad), precision=precision, device=0)

@@ -25,14 +25,14 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
           f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+CUDA_INC = Path(NVCC).resolve().parent.parent / "include"
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-v", "--expt-relaxed-constexpr",
-                            "-Xcompiler", "-Wall"]
+                            "-Xcompiler", "-Wall", f'-DTBN_CUDA_INC="{CUDA_INC}"']
 if os.environ.get("TBN_TRACE_BUILD"):          # development timeline build (see tools/trace_run.py)
     CU_FLAGS += ["-DTBN_ENABLE_TRACE"]
 if os.environ.get("TBN_EXTRA_FLAGS"):          # development A/B variants (tools/ab.sh)
     CU_FLAGS += os.environ["TBN_EXTRA_FLAGS"].split()
 CXX = shutil.which("g++") or "g++"
-CUDA_INC = Path(NVCC).resolve().parent.parent / "include"
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{CUDA_INC}"]
 
 
@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     newest = max(o.stat().st_mtime for o in objs)
     if force or not LIB.exists() or LIB.stat().st_mtime < newest:
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

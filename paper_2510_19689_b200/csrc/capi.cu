@@ -239,6 +239,7 @@ tbn_status tbn_model_create(const tbn_config* cfg, const char* const* names,
     if (!tbn::tc_pack(hp, precision, &m->tc, &err)) {
       cudaFree(m->d_simt);
       delete m;
+      if (err.rfind("unsupported:", 0) == 0) return fail(TBN_ERR_UNSUPPORTED, err);
       return fail(TBN_ERR_CUDA, "tcgen05 weight packing failed: " + err);
     }
   }
@@ -470,6 +471,10 @@ cudaError_t ensure(StreamCtx* c, size_t pin_bytes, size_t dev_bytes) {
     if (c->dev) cudaFree(c->dev);
     c->dev = nullptr; c->dev_bytes = 0;
     cudaError_t e = cudaMalloc(&c->dev, dev_bytes);
+    if (e != cudaSuccess) return e;
+    // defined contents for the alignment gaps the single-copy small-batch path
+    // moves along with the outputs (compute-sanitizer initcheck)
+    e = cudaMemset(c->dev, 0, dev_bytes);
     if (e != cudaSuccess) return e;
     c->dev_bytes = dev_bytes;
   }

@@ -28,10 +28,8 @@
 // Per-row arithmetic is identical for every row whatever the batch size, tile
 // position, grid or group: the batch-invariance contract (network.py:11-14).
 #pragma once
-#include <cstdint>
-#include <type_traits>
+#include "tbn_rtc.h"
 #include <cuda_bf16.h>
-#include <cuda_runtime.h>
 #include "tc_kernel.cuh"
 
 namespace tbn {
@@ -112,16 +110,7 @@ struct Cfg {
   // 4 slots (measured: 8 buys nothing and takes L1 away)
   static constexpr int NSLOT_FIT = RING ? cmin(4, (SMEM_MAX - FIX_S - STG_ALL) / HBR) : 0;
   static constexpr int NSLOT_SH = NSLOT_FIT >= 8 ? 8 : NSLOT_FIT >= 4 ? 4 : NSLOT_FIT >= 2 ? 2 : 0;  // power of 2
-  // per-group rings (GS slots each, no cross-group release protocol) when
-  // they fit: a shared ring ties every group to the slowest one
-#ifdef TBN_K2_GRING
-  static constexpr int GS_FIT = RING ? (SMEM_MAX - FIX_S - STG_ALL) / (NG * HBR) : 0;
-#else
-  static constexpr int GS_FIT = 0;
-#endif
-  static constexpr int GS = GS_FIT >= 3 ? 3 : GS_FIT;
-  static constexpr bool GRING = RING && GS >= 2;
-  static constexpr int NSLOT = GRING ? NG * GS : NSLOT_SH;   // slots in SMEM
+  static constexpr int NSLOT = NSLOT_SH;               // slots in SMEM
   static_assert(!RING || NSLOT >= 2, "not even a 2-slot weight ring fits");
   static_assert(NSLOT <= 16, "ring barriers");
   static constexpr int NB = 2 * (S + 1);               // ring blocks per tile: fc1_s, fc2_s
@@ -158,9 +147,13 @@ struct Bars {
 };
 
 __device__ __forceinline__ float tanh_approx(float x) {
+#ifdef TBN_K2_FAKETANH      // dev experiment only: how much of the time is the MUFU pipe
+  return fminf(fmaxf(x, -1.0f), 1.0f);
+#else
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+#endif
 }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
@@ -219,24 +212,15 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     const uint32_t i = v % NB;
     return p.wimg + ((i & 1) ? CF::O_FC2 : CF::O_FC1) + (i >> 1) * CF::HBR;
   };
-  // slot of block v: the CTA-wide ring, or this group's own GS slots (v is
-  // then the group's own block counter: its tiles are rounds 0, 1, ...)
-  auto ring_slot = [&](uint32_t v) -> int {
-    if constexpr (CF::GRING) return g * CF::GS + (int)(v % CF::GS);
-    else return (int)(v % NSLOT);
-  };
-  auto ring_parity = [&](uint32_t v) -> uint32_t {
-    if constexpr (CF::GRING) return (v / CF::GS) & 1u;
-    else return (v / NSLOT) & 1u;
-  };
+  // slot and phase parity of ring block v (v % NSLOT, use v / NSLOT);
+  // (measured and dropped: per-group 2-slot rings, 8% slower at 262,144 rows)
+  auto ring_slot = [&](uint32_t v) -> int { return NSLOT ? (int)(v % (NSLOT ? NSLOT : 1)) : 0; };
+  auto ring_parity = [&](uint32_t v) -> uint32_t { return NSLOT ? (v / (NSLOT ? NSLOT : 1)) & 1u : 0u; };
   auto ring_load = [&](uint32_t v) {
     const int sl = ring_slot(v);
     ptx::mbar_arrive_expect_tx(&bars->rfull[sl], CF::B_HID);
     ptx::bulk_g2s(smem + CF::OFF_RING + sl * CF::HBR, ring_src(v), CF::B_HID, &bars->rfull[sl]);
   };
-  // this group's tiles and ring blocks (per-group ring)
-  const int64_t rounds_g = tiles_cta > g ? (tiles_cta - g + NG - 1) / NG : 0;
-  const uint32_t nblk_g = (uint32_t)(rounds_g * NB);
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bars->cfull, 1);
@@ -262,18 +246,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       for (int o = 0; o < ATT_BYTES; o += CH)
         ptx::bulk_g2s(smem + CF::S_ATT + o, p.wimg + CF::O_ATT + o,
                       (uint32_t)(ATT_BYTES - o < CH ? ATT_BYTES - o : CH), &bars->cfull);
-      if constexpr (!CF::GRING)
-        for (uint32_t v = 0; v < (uint32_t)NSLOT && v < nblk; ++v) ring_load(v);
+      for (uint32_t v = 0; v < (uint32_t)NSLOT && v < nblk; ++v) ring_load(v);
     }
   }
   if (warp == 0) ptx::tmem_alloc<CF::TCOLS>(&bars->tmem_base);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if constexpr (CF::GRING) {      // each group's issuing thread primes its own ring
-    if ((warp & 3) == 0 && lane == 0)
-      for (uint32_t v = 0; v < (uint32_t)CF::GS && v < nblk_g; ++v) ring_load(v);
-  }
   const uint32_t tg = bars->tmem_base + (uint32_t)(g * CF::TCG) + ((uint32_t)(q * 32) << 16);
   const uint32_t tD = tg + CF::T_D, tA = tg + CF::T_A, tPR = tg + CF::T_PR;
   float* stg = reinterpret_cast<float*>(smem + CF::OFF_STG + warp * CF::STG);
@@ -324,6 +303,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       ptx::bulk_commit();
     }
     for (int e = nb + lane; e < ne; e += 32) dst[e] = stg[e];
+    __syncwarp();
   };
   auto claim_stg = [&]() {      // the previous bulk store has finished reading stg
     if (lane == 0) ptx::bulk_wait_read0();
@@ -333,9 +313,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   // release it refills its slot with block v + NSLOT.  Counters are monotonic:
   // use u = v / NSLOT of a slot completes at arrival (u + 1) * NG.
   auto ring_release = [&](uint32_t v) {
-    const uint32_t sl = v % NSLOT;
+    const uint32_t sl = (uint32_t)ring_slot(v);
     const uint32_t old = atomicAdd(&bars->rcnt[sl], 1u);
-    if (old == (v / NSLOT) * NG + NG - 1 && v + NSLOT < nblk) ring_load(v + NSLOT);
+    if (old == (v / (NSLOT ? NSLOT : 1)) * NG + NG - 1 && v + NSLOT < nblk) ring_load(v + NSLOT);
   };
 
   {   // this warp's first x tile streams in with the weights
@@ -360,24 +340,28 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   // block rv).  The group meets at its barrier, warp 0 of the group issues the
   // chain and commits it; `post` overlaps the MMA; then everyone waits for D.
   int jt = 0;                                    // trace: GEMM counter
-  int64_t ring_pending = -1;                     // ring block awaiting release (tr thread)
+  int64_t ring_pending = -1;                     // ring block awaiting release (same in every warp)
   const bool tr = (q == 0 && lane == 0);
   auto gemm = [&](int kind, uint32_t bo, int64_t rv, auto&& post) {
     if (tr) TBN_TRACE(g * 4000 + 4 * jt);
+    // the issuing warp rotates over the group's four warps (measured 1.3%
+    // faster at HR @ 65,536 than always warp 0: the issue work is spread)
+    const int iq = jt & 3;
     if constexpr (CF::RING) {
       // the issuing warp checks its ring block while the other warps finish
       // writing A (off the barrier -> MMA critical path)
       if (rv >= 0) {
         const uint32_t v = (uint32_t)rv;
-        if (q == 0) ptx::mbar_wait(&bars->rfull[ring_slot(v)], ring_parity(v));
+        if (q == iq) ptx::mbar_wait(&bars->rfull[ring_slot(v)], ring_parity(v));
         bo = CF::OFF_RING + ring_slot(v) * CF::HBR;
       }
     }
+    __syncwarp();                                  // bar.sync / tcgen05 .aligned: converged warp
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
     ptx::named_bar_sync(bar_id, 128);
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 1);
-    if (q == 0) {
+    if (q == iq) {
       ptx::tc_fence_after();
       const uint32_t tAL = tA + CF::KA;              // A_lo (3xTF32 only)
       if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tAL, wbase + bo);
@@ -387,17 +371,10 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       if constexpr (CF::RING) {
         // the previous GEMM's ring block: its MMAs completed before this chain
         // was issued, so release it now, off the critical path
-        if (lane == 0 && ring_pending >= 0) {
-          if constexpr (CF::GRING) {
-            const uint32_t v = (uint32_t)ring_pending + CF::GS;
-            if (v < nblk_g) ring_load(v);
-          } else {
-            ring_release((uint32_t)ring_pending);
-          }
-          ring_pending = -1;
-        }
+        if (ring_pending >= 0 && lane == 0) ring_release((uint32_t)ring_pending);
       }
     }
+    ring_pending = -1;         // every warp tracks the same block sequence
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 2);
     post();
     // every warp parks on the commit barrier (suspend-time hint: no spinning)
@@ -405,7 +382,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     dphase ^= 1;
     ptx::tc_fence_after();
     if constexpr (CF::RING) {
-      if (rv >= 0 && tr) ring_pending = rv;      // released under the next MMA chain
+      if (rv >= 0) ring_pending = rv;            // released under the next MMA chain
     }
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 3);
     ++jt;
@@ -473,13 +450,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     const int64_t m = g + (int64_t)NG * k;
     if (m >= tiles_cta) {
       // no tile for this group in the last round: release its ring blocks
-      if constexpr (CF::RING && !CF::GRING) {
+      if constexpr (CF::RING) {
         if (tr) {
           if (ring_pending >= 0) ring_release((uint32_t)ring_pending);
           ring_pending = -1;
           for (uint32_t i = 0; i < (uint32_t)NB; ++i) {
             const uint32_t v = (uint32_t)(k * NB) + i;
-            ptx::mbar_wait(&bars->rfull[v % NSLOT], (v / NSLOT) & 1u);
+            ptx::mbar_wait(&bars->rfull[ring_slot(v)], ring_parity(v));
             ring_release(v);
           }
         }
@@ -551,6 +528,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         if constexpr (F % 2) xv[F - 1] = (xv[F - 1] - cst[CF::C_SHIFT + F - 1]) * cst[CF::C_SCALE + F - 1];
       }
       if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
+      __syncwarp();
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         if constexpr (CF::XS) my_xs[f] = xv[f];
@@ -629,6 +607,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       }
 #pragma unroll
       for (int f = 0; f < F; ++f) agg[f] = fmaf(w, my_stg[f], agg[f]);
+      __syncwarp();
     };
 
     transform(0, nopost);                                        // network.py:226-227
@@ -711,12 +690,18 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
             sm = fmaf(mk, z[F - 1], sm);
             cn += mk;
           }
+#ifdef TBN_K2_FAKEMICH      // dev experiment only: the cost of the Michelot passes
+          if (it >= 1) break;
+#endif
           if (cn >= cnt_prev) break;
           cnt_prev = cn;
           // sparsemax.py:39: (sum - 1) / k as (sum - 1) * rcp_rn(k), k from the
           // table (one rounding per operation: the emulation oracle repeats it)
           tau = (sm - 1.0f) * rcp_tab[(int)cn];
         }
+        // the lanes left the loop at different passes: reconverge before the
+        // warp-collective (.aligned) tcgen05 loads/stores and named barriers
+        __syncwarp();
       }
       // mask, prior update, x*mask -> A (elements 2 ..); mask -> staging
       // (network.py:236-238, :246), in 16-feature chunks
@@ -807,7 +792,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     }
     if (tr) TBN_TRACE(g * 4000 + 3003 + 8 * (int)k);
   }
-  if constexpr (CF::RING && !CF::GRING) {
+  if constexpr (CF::RING) {
     if (tr && ring_pending >= 0) ring_release((uint32_t)ring_pending);
   }
   if (lane == 0) ptx::bulk_wait0();

@@ -19,28 +19,21 @@
 
 namespace tbn {
 
-namespace {
-
-struct K2Instance {
-  int F, ND, NA, S, C, prec;
-  bool (*pack)(const HostParams&, TcModel*, std::string*);
-  cudaError_t (*launch)(const TcModel&, const ForwardArgs&, int, cudaStream_t);
-};
-
-template <class CF>
-bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
-  constexpr int F = CF::F, H = CF::H, N2 = CF::N2, S = CF::S, ND = CF::ND, NA = CF::NA, C = CF::C;
-  std::vector<float> img(CF::IMG_BYTES / 4, 0.0f);
+// The K2 weight image for one shape (layout L): constants, then every B
+// operand block (pack_util.h: N x K K-major canonical, bias hi/lo rows 0/1).
+bool k2_pack_layout(const K2Layout& L, const HostParams& hp, TcModel* out, std::string* err) {
+  const int F = L.F, H = L.H, N2 = L.N2, S = L.S, ND = L.ND, NA = L.NA, C = L.C;
+  std::vector<float> img(L.IMG_BYTES / 4, 0.0f);
   for (int f = 0; f < F; ++f) {
-    img[CF::C_SCALE + f] = (float)(1.0 / std::sqrt(hp.norm_var[f] + 1e-8));   // network.py:120
-    img[CF::C_SHIFT + f] = (float)hp.norm_mean[f];
+    img[L.C_SCALE + f] = (float)(1.0 / std::sqrt(hp.norm_var[f] + 1e-8));   // network.py:120
+    img[L.C_SHIFT + f] = (float)hp.norm_mean[f];
   }
-  for (int i = 0; i < ND * C; ++i) img[CF::C_HW + i] = (float)hp.head_W[i];
-  for (int i = 0; i < C; ++i) img[CF::C_HB + i] = (float)hp.head_b[i];
+  for (int i = 0; i < ND * C; ++i) img[L.C_HW + i] = (float)hp.head_W[i];
+  for (int i = 0; i < C; ++i) img[L.C_HB + i] = (float)hp.head_b[i];
   const double kR = 0.70710678118654752440, kLog2e = 1.4426950408889634;
   std::vector<double> cs_first(N2), cs_res(N2);
   for (int n = 0; n < N2; ++n) {
-    if (CF::X3) {            // exact sigmoid: gate x -log2(e); residual linear x sqrt(.5)
+    if (L.X3) {              // exact sigmoid: gate x -log2(e); residual linear x sqrt(.5)
       cs_first[n] = n < H ? 1.0 : -kLog2e;
       cs_res[n] = n < H ? kR : -kLog2e;
     } else {                 // tanh form: everything x 1/2, residual linear x sqrt(.5)/2
@@ -49,30 +42,58 @@ bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
     }
   }
   using pack::pack_block_k2;
-  constexpr int HB = tc::rup(CF::B_HID, 128);
-  pack_block_k2(img, CF::O_SH1 / 4, hp.sh1_W, F, N2, N2, CF::K1, CF::X3, N2, &cs_first, hp.sh1_b, CF::BF);
-  pack_block_k2(img, CF::O_SH2 / 4, hp.sh2_W, H, N2, N2, CF::KHID, CF::X3, N2, &cs_res, hp.sh2_b, CF::BF);
+  pack_block_k2(img, L.O_SH1 / 4, hp.sh1_W, F, N2, N2, L.K1, L.X3, N2, &cs_first, hp.sh1_b, L.BF);
+  pack_block_k2(img, L.O_SH2 / 4, hp.sh2_W, H, N2, N2, L.KHID, L.X3, N2, &cs_res, hp.sh2_b, L.BF);
   for (int s = 0; s <= S; ++s) {
-    pack_block_k2(img, (CF::O_FC1 + s * HB) / 4, hp.fc1_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
-                  hp.fc1_b[s], CF::BF);
-    pack_block_k2(img, (CF::O_FC2 + s * HB) / 4, hp.fc2_W[s], H, N2, N2, CF::KHID, CF::X3, N2, &cs_res,
-                  hp.fc2_b[s], CF::BF);
+    pack_block_k2(img, (L.O_FC1 + s * L.HBR) / 4, hp.fc1_W[s], H, N2, N2, L.KHID, L.X3, N2, &cs_res,
+                  hp.fc1_b[s], L.BF);
+    pack_block_k2(img, (L.O_FC2 + s * L.HBR) / 4, hp.fc2_W[s], H, N2, N2, L.KHID, L.X3, N2, &cs_res,
+                  hp.fc2_b[s], L.BF);
   }
   for (int s = 1; s <= S; ++s)
-    pack_block_k2(img, (CF::O_ATT + (s - 1) * tc::rup(CF::B_ATT, 128)) / 4, hp.att_W[s], NA, F, CF::FN,
-                  CF::KATT, CF::X3, F, nullptr, hp.att_b[s], CF::BF);
+    pack_block_k2(img, (L.O_ATT + (s - 1) * L.ABR) / 4, hp.att_W[s], NA, F, L.FN, L.KATT, L.X3, F, nullptr,
+                  hp.att_b[s], L.BF);
   void* d = nullptr;
-  cudaError_t e = cudaMalloc(&d, CF::IMG_BYTES);
-  if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), CF::IMG_BYTES, cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMalloc(&d, L.IMG_BYTES);
+  if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), L.IMG_BYTES, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     if (d) cudaFree(d);
     if (err) *err = cudaGetErrorString(e);
     return false;
   }
   out->d_buf = d;
-  out->bytes = CF::IMG_BYTES;
+  out->bytes = L.IMG_BYTES;
   out->params = new k2::Params{(const uint8_t*)d, (float)hp.gamma};
   return true;
+}
+
+namespace {
+
+struct K2Instance {
+  int F, ND, NA, S, C, prec;
+  bool (*pack)(const HostParams&, TcModel*, std::string*);
+  cudaError_t (*launch)(const TcModel&, const ForwardArgs&, int, cudaStream_t);
+};
+
+// Everything the packer and the launcher need to know about one K2 shape;
+// built from the compile-time Cfg for the prebuilt instances and read back
+// from a query kernel for NVRTC-compiled ones (kernel_k2_jit.cu).
+template <class CF>
+K2Layout layout_of() {
+  K2Layout L;
+  L.F = CF::F; L.ND = CF::ND; L.NA = CF::NA; L.S = CF::S; L.C = CF::C;
+  L.X3 = CF::X3; L.BF = CF::BF; L.H = CF::H; L.N2 = CF::N2;
+  L.K1 = CF::K1; L.KHID = CF::KHID; L.KATT = CF::KATT; L.FN = CF::FN;
+  L.C_SCALE = CF::C_SCALE; L.C_SHIFT = CF::C_SHIFT; L.C_HW = CF::C_HW; L.C_HB = CF::C_HB;
+  L.O_SH1 = CF::O_SH1; L.O_SH2 = CF::O_SH2; L.O_FC1 = CF::O_FC1; L.O_FC2 = CF::O_FC2; L.O_ATT = CF::O_ATT;
+  L.HBR = tc::rup(CF::B_HID, 128); L.ABR = tc::rup(CF::B_ATT, 128);
+  L.IMG_BYTES = CF::IMG_BYTES; L.SMEM_BYTES = CF::SMEM_BYTES; L.THREADS = CF::THREADS;
+  return L;
+}
+
+template <class CF>
+bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
+  return k2_pack_layout(layout_of<CF>(), hp, out, err);
 }
 
 template <class CF>
@@ -132,6 +153,7 @@ bool k2_pack(const HostParams& hp, int precision, TcModel* out, std::string* err
     return false;
   }
   out->shape_id = (int)(in - kK2);
+  out->jit = nullptr;
   return in->pack(hp, out, err);
 }
 
@@ -143,6 +165,7 @@ void k2_free(TcModel* m) {
 }
 
 cudaError_t k2_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  if (m.jit) return k2_jit_launch(m, a, num_sms, stream);
   if (m.shape_id < 0) return cudaErrorInvalidValue;
   return kK2[m.shape_id].launch(m, a, num_sms, stream);
 }

@@ -1,0 +1,313 @@
+// kernel_k2_jit.cu — K2 for any model shape: the same kernel template
+// (k2_kernel.cuh) compiled at model creation with NVRTC for the model's
+// (F, n_d, n_a, n_steps, C, precision) when no prebuilt instance exists
+// (the paper's own model F=35/n_d=n_a=8/S=3, a one-hot HR model F=52, ...).
+//
+// * NVRTC is loaded lazily (dlopen), so the library still loads without it;
+//   TBN_NO_JIT=1 disables the path.  The kernel headers are read from the
+//   csrc/ directory next to this library (they travel with it).
+// * The program holds the kernel instantiation and a one-thread layout query
+//   kernel that reports the shape's Cfg constants, so the host packer
+//   (k2_pack_layout) uses exactly the offsets the kernel was compiled with.
+// * cubins are cached per (shape, precision, header contents) in memory and
+//   on disk ($TBN_JIT_CACHE, else ~/.cache/tabnet_b200).
+// * A shape the kernel's static limits reject (TMEM columns, shared memory,
+//   MMA N <= 256) fails the compile: the model reports UNSUPPORTED and
+//   precision="auto" falls back to the CUDA-core kernel.
+#include <dlfcn.h>
+#include <sys/stat.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "k2_kernel.cuh"
+#include "tbn_tc.h"
+
+#ifndef TBN_CUDA_INC
+#define TBN_CUDA_INC "/usr/local/cuda/include"
+#endif
+
+namespace tbn {
+namespace {
+
+// ---- NVRTC, resolved at run time ------------------------------------------
+struct Nvrtc {
+  typedef int (*Create)(void**, const char*, const char*, int, const char* const*, const char* const*);
+  typedef int (*Compile)(void*, int, const char* const*);
+  typedef int (*Size)(void*, size_t*);
+  typedef int (*Get)(void*, char*);
+  typedef int (*AddName)(void*, const char*);
+  typedef int (*Lowered)(void*, const char*, const char**);
+  typedef int (*Destroy)(void**);
+  Create create = nullptr;
+  Compile compile = nullptr;
+  Size log_size = nullptr, cubin_size = nullptr;
+  Get log = nullptr, cubin = nullptr;
+  AddName add_name = nullptr;
+  Lowered lowered = nullptr;
+  Destroy destroy = nullptr;
+  bool ok = false;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (const char* off = std::getenv("TBN_NO_JIT"))
+      if (off[0] && off[0] != '0') return;
+    const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"};
+    void* h = nullptr;
+    for (const char* nm : names)
+      if ((h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+    if (!h) return;
+    n.create = (Nvrtc::Create)dlsym(h, "nvrtcCreateProgram");
+    n.compile = (Nvrtc::Compile)dlsym(h, "nvrtcCompileProgram");
+    n.log_size = (Nvrtc::Size)dlsym(h, "nvrtcGetProgramLogSize");
+    n.log = (Nvrtc::Get)dlsym(h, "nvrtcGetProgramLog");
+    n.cubin_size = (Nvrtc::Size)dlsym(h, "nvrtcGetCUBINSize");
+    n.cubin = (Nvrtc::Get)dlsym(h, "nvrtcGetCUBIN");
+    n.add_name = (Nvrtc::AddName)dlsym(h, "nvrtcAddNameExpression");
+    n.lowered = (Nvrtc::Lowered)dlsym(h, "nvrtcGetLoweredName");
+    n.destroy = (Nvrtc::Destroy)dlsym(h, "nvrtcDestroyProgram");
+    n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.add_name &&
+           n.lowered && n.destroy;
+  });
+  return n;
+}
+
+// directory of this shared library (its csrc/ holds the kernel headers)
+std::string lib_dir() {
+  Dl_info info{};
+  if (dladdr((void*)&lib_dir, &info) && info.dli_fname) {
+    std::string p = info.dli_fname;
+    const size_t s = p.rfind('/');
+    return s == std::string::npos ? std::string(".") : p.substr(0, s);
+  }
+  return ".";
+}
+
+std::string read_file(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+const char* kHeaders[] = {"k2_kernel.cuh", "tc_kernel.cuh", "tc_ptx.cuh", "tbn_rtc.h", "tbn_args.h"};
+constexpr int kLayoutInts = 27;
+
+struct JitK2 {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  K2Layout L;
+  std::mutex attr_mu;
+  bool attr_set[kMaxDevices] = {};
+};
+
+std::mutex g_mu;
+std::map<std::string, std::unique_ptr<JitK2>> g_cache;
+
+std::string cache_dir() {
+  if (const char* d = std::getenv("TBN_JIT_CACHE")) return d;
+  if (const char* x = std::getenv("XDG_CACHE_HOME")) return std::string(x) + "/tabnet_b200";
+  if (const char* home = std::getenv("HOME")) return std::string(home) + "/.cache/tabnet_b200";
+  return "/tmp/tabnet_b200";
+}
+
+void mkdirs(const std::string& d) {
+  std::string cur;
+  for (size_t i = 0; i <= d.size(); ++i) {
+    if (i == d.size() || d[i] == '/') {
+      if (!cur.empty()) mkdir(cur.c_str(), 0755);
+    }
+    if (i < d.size()) cur.push_back(d[i]);
+  }
+}
+
+// NVRTC-compile the K2 instance + layout query for one shape; returns the cubin
+bool compile(const std::string& src, const std::string& kname, std::vector<char>* cubin, std::string* lowered,
+             std::string* log_out) {
+  const Nvrtc& nv = nvrtc();
+  void* prog = nullptr;
+  if (nv.create(&prog, src.c_str(), "tbn_k2_jit.cu", 0, nullptr, nullptr) != 0) {
+    *log_out = "nvrtcCreateProgram failed";
+    return false;
+  }
+  nv.add_name(prog, kname.c_str());
+  const std::string inc_csrc = "-I" + lib_dir() + "/csrc";
+  const char* cuda_inc_env = std::getenv("TBN_CUDA_INC");
+  const std::string inc_cuda = std::string("-I") + (cuda_inc_env ? cuda_inc_env : TBN_CUDA_INC);
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "-DTBN_NVRTC",
+                        inc_csrc.c_str(), inc_cuda.c_str(), "-diag-suppress=179,39,549"};
+  const int rc = nv.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  size_t ls = 0;
+  nv.log_size(prog, &ls);
+  std::string log(ls, '\0');
+  if (ls) nv.log(prog, &log[0]);
+  *log_out = log;
+  bool ok = rc == 0;
+  if (ok) {
+    size_t n = 0;
+    nv.cubin_size(prog, &n);
+    cubin->resize(n);
+    nv.cubin(prog, cubin->data());
+    const char* low = nullptr;
+    ok = nv.lowered(prog, kname.c_str(), &low) == 0 && low;
+    if (ok) *lowered = low;
+  }
+  nv.destroy(&prog);
+  return ok;
+}
+
+JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
+  const std::string dir = lib_dir() + "/csrc/";
+  std::string hdrs;
+  for (const char* h : kHeaders) hdrs += read_file(dir + h);
+  if (hdrs.empty()) {
+    *err = "unsupported: kernel headers not found in " + dir;
+    return nullptr;
+  }
+  char shape[128];
+  std::snprintf(shape, sizeof(shape), "%d, %d, %d, %d, %d, %d", hp.F, hp.ND, hp.NA, hp.S, hp.C, prec);
+  const std::string cfg = std::string("tbn::k2::Cfg<") + shape + ">";
+  const std::string kname = "tbn::k2::tabnet_rowthread<" + cfg + ">";
+  std::ostringstream src;
+  src << "#include \"k2_kernel.cuh\"\n"
+      << "typedef " << cfg << " JCF;\n"
+      << "template __global__ void tbn::k2::tabnet_rowthread<JCF>(tbn::k2::Params, tbn::ForwardArgs);\n"
+      << "extern \"C\" __global__ void tbn_k2_layout(int* o) {\n"
+      << "  const int v[] = {JCF::F, JCF::ND, JCF::NA, JCF::S, JCF::C, JCF::X3, JCF::BF, JCF::H, JCF::N2,\n"
+      << "    JCF::K1, JCF::KHID, JCF::KATT, JCF::FN, JCF::C_SCALE, JCF::C_SHIFT, JCF::C_HW, JCF::C_HB,\n"
+      << "    JCF::O_SH1, JCF::O_SH2, JCF::O_FC1, JCF::O_FC2, JCF::O_ATT, tbn::tc::rup(JCF::B_HID, 128),\n"
+      << "    tbn::tc::rup(JCF::B_ATT, 128), JCF::IMG_BYTES, JCF::SMEM_BYTES, JCF::THREADS};\n"
+      << "  for (int i = 0; i < " << kLayoutInts << "; ++i) o[i] = v[i];\n}\n";
+  const std::string source = src.str();
+  const std::string key = source + "|" + hdrs;
+
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) return it->second.get();
+
+  char hex[32];
+  std::snprintf(hex, sizeof(hex), "%016llx", (unsigned long long)fnv1a(key));
+  const std::string cdir = cache_dir();
+  const std::string cpath = cdir + "/k2_" + hex + ".cubin", npath = cdir + "/k2_" + hex + ".name";
+  std::vector<char> cubin;
+  std::string lowered;
+  {
+    const std::string c = read_file(cpath), nm = read_file(npath);
+    if (!c.empty() && !nm.empty()) {
+      cubin.assign(c.begin(), c.end());
+      lowered = nm;
+    }
+  }
+  if (cubin.empty()) {
+    if (!nvrtc().ok) {
+      *err = "unsupported: no prebuilt K2 instance for this shape and NVRTC is unavailable";
+      return nullptr;
+    }
+    std::string log;
+    if (!compile(source, kname, &cubin, &lowered, &log)) {
+      *err = "unsupported: K2 does not compile for this shape: " + log.substr(0, 600);
+      return nullptr;
+    }
+    mkdirs(cdir);
+    std::ofstream(cpath, std::ios::binary).write(cubin.data(), (std::streamsize)cubin.size());
+    std::ofstream(npath, std::ios::binary) << lowered;
+  }
+  std::unique_ptr<JitK2> j(new JitK2());
+  cudaError_t e = cudaLibraryLoadData(&j->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&j->kern, j->lib, lowered.c_str());
+  cudaKernel_t q = nullptr;
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&q, j->lib, "tbn_k2_layout");
+  int* d = nullptr;
+  int h[kLayoutInts] = {};
+  if (e == cudaSuccess) e = cudaMalloc(&d, sizeof(h));
+  if (e == cudaSuccess) {
+    void* args[] = {&d};
+    e = cudaLaunchKernel((const void*)q, dim3(1), dim3(1), args, 0, nullptr);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  if (d) cudaFree(d);
+  if (e != cudaSuccess) {
+    *err = std::string("JIT K2 load: ") + cudaGetErrorString(e);
+    if (j->lib) cudaLibraryUnload(j->lib);
+    return nullptr;
+  }
+  K2Layout& L = j->L;
+  int i = 0;
+  L.F = h[i++]; L.ND = h[i++]; L.NA = h[i++]; L.S = h[i++]; L.C = h[i++];
+  L.X3 = h[i++] != 0; L.BF = h[i++] != 0; L.H = h[i++]; L.N2 = h[i++];
+  L.K1 = h[i++]; L.KHID = h[i++]; L.KATT = h[i++]; L.FN = h[i++];
+  L.C_SCALE = h[i++]; L.C_SHIFT = h[i++]; L.C_HW = h[i++]; L.C_HB = h[i++];
+  L.O_SH1 = h[i++]; L.O_SH2 = h[i++]; L.O_FC1 = h[i++]; L.O_FC2 = h[i++]; L.O_ATT = h[i++];
+  L.HBR = h[i++]; L.ABR = h[i++]; L.IMG_BYTES = h[i++]; L.SMEM_BYTES = h[i++]; L.THREADS = h[i++];
+  JitK2* raw = j.get();
+  g_cache[key] = std::move(j);
+  return raw;
+}
+
+int tc_prec(int precision) {
+  return precision == 0 ? tc::kPrecTF32x3 : precision == 1 ? tc::kPrecTF32 : precision == 2 ? tc::kPrecBF16 : -1;
+}
+
+}  // namespace
+
+bool k2_jit_available() { return nvrtc().ok; }
+
+bool k2_jit_pack(const HostParams& hp, int precision, TcModel* out, std::string* err) {
+  const int prec = tc_prec(precision);
+  if (prec < 0) {
+    if (err) *err = "unsupported: precision";
+    return false;
+  }
+  std::string e;
+  JitK2* j = get_or_build(hp, prec, &e);
+  if (!j) {
+    if (err) *err = e;
+    return false;
+  }
+  out->kernel = 2;
+  out->precision = precision;
+  out->shape_id = -1;
+  out->jit = j;
+  return k2_pack_layout(j->L, hp, out, err);
+}
+
+cudaError_t k2_jit_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  JitK2* j = const_cast<JitK2*>(static_cast<const JitK2*>(m.jit));
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  {
+    std::lock_guard<std::mutex> lk(j->attr_mu);
+    if (!j->attr_set[dev]) {
+      e = cudaFuncSetAttribute((const void*)j->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, j->L.SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      j->attr_set[dev] = true;
+    }
+  }
+  // the same geometry as the prebuilt instances (kernel_k2.cu launch_k2_impl)
+  const int64_t nq = (a.rows + 127) / 128;
+  const int grid = (int)(nq < num_sms ? nq : num_sms);
+  k2::Params p = *(const k2::Params*)m.params;
+  ForwardArgs fa = a;
+  void* args[] = {&p, &fa};
+  return cudaLaunchKernel((const void*)j->kern, dim3(grid), dim3(j->L.THREADS), args, j->L.SMEM_BYTES, stream);
+}
+
+}  // namespace tbn

@@ -138,7 +138,10 @@ const Instance* find(const HostParams& hp, int precision) {
 }  // namespace
 
 bool tc_supported(const HostParams& hp, int precision) {
-  return k3_supported(hp, precision) || k2_supported(hp, precision) || find(hp, precision) != nullptr;
+  // prebuilt instances, else K2 compiled for the shape at model creation
+  // (whether that compile succeeds is only known then: tc_pack reports it)
+  return k3_supported(hp, precision) || k2_supported(hp, precision) || find(hp, precision) != nullptr ||
+         (k2_jit_available() && precision >= 0 && precision <= 2);
 }
 
 // K2 (k2_kernel.cuh) serves the single-pass modes wherever an instance exists;
@@ -161,7 +164,8 @@ bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err
   }
   const Instance* in = find(hp, precision);
   if (!in) {
-    if (err) *err = "no instance";
+    if (k2_allowed() && k2_jit_available()) return k2_jit_pack(hp, precision, out, err);
+    if (err) *err = "unsupported: no kernel instance for this shape";
     return false;
   }
   out->kernel = 1;

@@ -4,6 +4,7 @@
 #include <mutex>
 #include <string>
 #include <cuda_runtime.h>
+#include "tbn_args.h"
 
 namespace tbn {
 
@@ -43,21 +44,6 @@ struct SimtParams {
   const float* head_W; const float* head_b; // (ND,C) (C)
 };
 
-struct ForwardArgs {
-  const float* x;
-  int64_t rows;
-  int normalized;
-  const float* scale;   // per-call override (batch-stats control); null = model's
-  const float* shift;
-  float* logits;
-  float* probs;
-  float* masks;
-  float* importance;
-  int32_t* pred;
-  int32_t* err_flag;
-  float* scratch;              // K3: per-CTA row-tile state in the workspace
-  unsigned long long* trace;   // debug timeline (TBN_TRACE env); null in production
-};
 
 size_t simt_smem_bytes(const SimtParams& p);
 bool simt_supported(int F, int H, int C);      // the CUDA-core kernel's shape limits

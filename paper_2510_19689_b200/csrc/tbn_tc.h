@@ -29,7 +29,19 @@ struct TcModel {
   size_t bytes = 0;
   size_t scratch_per_cta = 0;   // K3: global per-CTA row-tile state (prior, agg, mask)
   void* params = nullptr;  // host copy of the kernel's parameter block
+  const void* jit = nullptr;    // K2 compiled at run time (kernel_k2_jit.cu), else null
 };
+
+// A K2 shape's image/launch layout (k2_kernel.cuh Cfg constants, at run time).
+struct K2Layout {
+  int F = 0, ND = 0, NA = 0, S = 0, C = 0;
+  bool X3 = false, BF = false;
+  int H = 0, N2 = 0, K1 = 0, KHID = 0, KATT = 0, FN = 0;
+  int C_SCALE = 0, C_SHIFT = 0, C_HW = 0, C_HB = 0;
+  int O_SH1 = 0, O_SH2 = 0, O_FC1 = 0, O_FC2 = 0, O_ATT = 0, HBR = 0, ABR = 0;
+  int IMG_BYTES = 0, SMEM_BYTES = 0, THREADS = 0;
+};
+bool k2_pack_layout(const K2Layout& L, const HostParams& hp, TcModel* out, std::string* err);
 
 bool tc_supported(const HostParams& hp, int precision);
 bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
@@ -41,6 +53,12 @@ bool k2_supported(const HostParams& hp, int precision);
 bool k2_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
 void k2_free(TcModel* m);
 cudaError_t k2_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream);
+
+// K2 compiled for the model's shape at run time with NVRTC (kernel_k2_jit.cu):
+// any shape the kernel's static limits admit, cubins cached in memory and on disk
+bool k2_jit_available();
+bool k2_jit_pack(const HostParams& hp, int precision, TcModel* out, std::string* err);
+cudaError_t k2_jit_launch(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream);
 
 // K3, the wide-model design (kernel_k3.cu)
 bool k3_supported(const HostParams& hp, int precision);

@@ -24,12 +24,10 @@
 // Per-row arithmetic is identical for every row whatever the batch size, tile
 // position, grid size or group: the batch-invariance contract (network.py:11-14).
 #pragma once
-#include <cstdint>
-#include <type_traits>
+#include "tbn_rtc.h"
 #include <cuda_bf16.h>
-#include <cuda_runtime.h>
 #include "tc_ptx.cuh"
-#include "tbn_internal.h"
+#include "tbn_args.h"
 
 namespace tbn {
 namespace tc {
@@ -898,6 +896,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
               cnt_prev = c;
               tau = __fdividef(sm - 1.0f, c);                         // sparsemax.py:39
             }
+            __syncwarp();                     // lanes left the search at different passes
             send_tau(zmax, tau);                                     // -> half 1
           } else {
             agg_half1();                                             // in the tau search's shadow

@@ -2,8 +2,7 @@
 // copies (TMA engine), TMEM allocation, tcgen05.mma/commit/ld/st and the UMMA
 // shared-memory / instruction descriptors (canonical K-major, no swizzle).
 #pragma once
-#include <cstdint>
-#include <cuda_runtime.h>
+#include "tbn_rtc.h"
 
 namespace tbn {
 namespace ptx {
@@ -23,6 +22,13 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ---- mbarrier -------------------------------------------------------------
+// TBN_WAIT_BRA: the retry branch of the try_wait loops (dev A/B: "bra.uni"
+// asserts a warp-uniform outcome, plain "bra" lets lanes leave separately)
+#ifdef TBN_WAIT_NOUNI
+#define TBN_WAIT_BRA "bra"
+#else
+#define TBN_WAIT_BRA "bra.uni"
+#endif
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -43,7 +49,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n\t.reg .pred P1;\n\t"
       "TBN_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra.uni TBN_WAIT_%=;\n\t}"
+      "@!P1 " TBN_WAIT_BRA " TBN_WAIT_%=;\n\t}"
       ::"r"(smem_u32(bar)), "r"(parity)
       : "memory");
 }
@@ -55,7 +61,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "{\n\t.reg .pred P1;\n\t"
       "TBN_WAITS_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra.uni TBN_WAITS_%=;\n\t}"
+      "@!P1 " TBN_WAIT_BRA " TBN_WAITS_%=;\n\t}"
       ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
       : "memory");
 }
@@ -221,12 +227,18 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Named barrier among `nthreads` threads (ids 1.. ; 0 is __syncthreads).
+// barrier.sync (not bar.sync = barrier.sync.aligned): correct even when the
+// lanes of a warp arrive separately after a data-dependent loop; the
+// __syncwarp also reconverges them for the .aligned tcgen05 ops that follow.
+// (compute-sanitizer synccheck flagged the .aligned form; same speed.)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 // Arrive without waiting (producer side of a named-barrier handoff).
 __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  __syncwarp();
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace ptx

@@ -575,3 +575,51 @@ def test_device_model_from_tbnt_stream(precision):
     bad[50] ^= 1
     with pytest.raises(P.ChecksumError):
         PIO.load_device_model(bytes(bad), precision=precision, device=0)
+
+
+def _shape_model(F, nd, na, S, C, precision, seed=0):
+    cfg = P.ModelConfig(feature_count=F, n_classes=C, n_d=nd, n_a=na, n_steps=S, seed=seed)
+    p = P.init_parameters(cfg)
+    for k in list(p):
+        if k.endswith("_att_W"):
+            p[k] = p[k] * 16.0
+    p["head_W"] = p["head_W"] * 8.0
+    rng = np.random.default_rng(seed + 3)
+    return P.TabNetModel(config=cfg, params=p, norm_mean=rng.standard_normal(F), norm_var=rng.uniform(0.5, 2.0, F),
+                         model_version=f"jit{F}", precision=precision)
+
+
+@pytest.mark.parametrize("precision", ["tf32x3", "bf16", "tf32"])
+@pytest.mark.parametrize("shape", [(35, 8, 8, 3, 2), (52, 8, 8, 3, 2), (20, 12, 4, 4, 3)])
+def test_runtime_compiled_k2_shapes(shape, precision):
+    """Shapes without a prebuilt instance run K2 compiled at model creation
+    (NVRTC, kernel_k2_jit.cu): the paper's own model (F=35, n_d=n_a=8, S=3,
+    PAPER.md:179), a one-hot HR model (F=52) and an
+    asymmetric n_d != n_a, 3-class shape.  3xTF32 against the float64 oracle
+    under the tie-aware rule; bf16/tf32 against the rounding-faithful emulation."""
+    from oracle import tabnet_emulate as E
+    F, nd, na, S, C = shape
+    m = _shape_model(F, nd, na, S, C, precision)
+    eng = m.engine()
+    assert eng.precision == precision                       # a tensor-core kernel, no fallback
+    x = W.make_inputs(W.Workload("jit", 9, F, nd, na, S, C, 0, "jit"), 1500)
+    r = m.apply(x.astype(np.float64))
+    if precision == "tf32x3":
+        ref = O.apply_model(m, x.astype(np.float64), diagnostics=True)
+        zs, tau = ref["z_shift"], ref["tau"]
+        ref["margin"] = np.abs(zs - tau[..., None]).min(axis=2) / np.maximum(np.abs(zs).max(axis=2), 1e-300)
+        p = np.sort(ref["probabilities"], axis=1)
+        ref["top2_gap"] = p[:, -1] - p[:, -2]
+        rep = compare(ref, _res_dict(r))
+        print(shape, precision, rep.summary())
+        assert rep.ok, rep.summary()
+        assert len(rep.exempt_rows) < 1500 // 20
+    else:
+        emu = E.apply_model_emulated(m, x, mode=precision)
+        st = _emu_stats(_res_dict(r), emu)
+        print(shape, precision, st)
+        mmax, mp999, imax, pmax = EMU_BOUNDS[precision]
+        assert st["mask_max"] < mmax and st["mask_p999"] < mp999 and st["imp_max"] < imax and st["prob_max"] < pmax
+    # batch invariance holds for the compiled-at-run-time kernel as well
+    part = m.apply(x[:333].astype(np.float64))
+    assert np.array_equal(part.masks, r.masks[:, :333]) and np.array_equal(part.probabilities, r.probabilities[:333])

@@ -1,0 +1,41 @@
+"""One small forward of every kernel instance (K1/K2/K3/CUDA-core, the
+standalone sparsemax, batch statistics, partition means, preprocessing) for
+compute-sanitizer runs (tools/sanitize.sh).  Rows span a partial tile and a
+CTA with warps without rows."""
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+import paper_2510_19689_b200 as P
+from paper_2510_19689_b200 import workloads as W
+from paper_2510_19689_b200.device import DeviceRunner
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+cases = [("adult", "bf16"), ("adult", "tf32x3"), ("hr", "bf16"), ("hr", "tf32"), ("hr", "tf32x3"),
+         ("bls", "bf16"), ("bls", "tf32x3"), ("bls", "tf32"), ("wide", "bf16"), ("hr", "fp32"), ("wide", "fp32")]
+for name, prec in cases:
+    if which != "all" and which != f"{name}/{prec}":
+        continue
+    m = W.make_engine_model(name, "trained", precision=prec, device=0)
+    rows = 300 if name != "wide" else 160
+    r = DeviceRunner(m, rows, device=0)
+    x = torch.from_numpy(W.make_inputs(W.WORKLOADS[name], rows)).cuda()
+    r.run(x)
+    torch.cuda.synchronize()
+    r.check_finite()
+    m.apply(x[:37].double().cpu().numpy(), use_batch_stats=True)   # batch-stats kernel + host path
+    print("ok", name, prec, flush=True)
+    del r, m
+if which in ("all", "aux"):
+    print(P.sparsemax(np.random.default_rng(0).standard_normal((100, 35))).shape)
+    from paper_2510_19689_b200 import interpret
+    m = W.make_engine_model("hr", "trained", precision="bf16", device=0)
+    interpret.stability_score(m, W.make_inputs(W.WORKLOADS["hr"], 400).astype(np.float64), 4)
+    print("ok aux", flush=True)
+import gc
+for k in list(globals()):
+    if k in ("m", "r", "x"):
+        del globals()[k]
+gc.collect()
+torch.cuda.synchronize()
+torch.cuda.empty_cache()

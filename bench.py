@@ -339,16 +339,23 @@ def run_reference(a) -> None:
 
 
 # ----------------------------------------------------------------------------- GPU arm
-def profile_traffic(config: str, precision: str):
+def profile_traffic(config: str, precision: str, rows: int):
+    """DRAM read+write bytes per launch of `rows` rows from the committed ncu
+    captures: the steady-state capture (tools/profile_traffic.sh: application
+    replay, no cache control, inside a rotating > L2 launch sequence) scaled
+    per row, else the single-launch --set full figure."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
-        return None
+        return None, None
     try:
         d = json.loads(p.read_text())
-        e = d.get(f"{config}/{precision}")
-        return e.get("dram_bytes_per_launch") if e else None
+        e = d.get(f"{config}/{precision}") or {}
+        if "dram_bytes_per_row_steady" in e:
+            return e["dram_bytes_per_row_steady"] * rows, e.get("steady_how")
+        v = e.get("dram_bytes_per_launch")
+        return v, ("single --set full launch (outputs left in L2: under-counts writes)" if v else None)
     except Exception:
-        return None
+        return None, None
 
 
 def roofline(precision: str, counts: dict, rows: int, kernel_ms: float, peaks: dict) -> dict:
@@ -599,8 +606,8 @@ def run_ours(a) -> None:
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     roof = roofline(a.precision, counts, sr.chunk, kernel_ms, peaks)
-    roof["traffic"] = profile_traffic(a.config, a.precision)
-    roof["traffic_source"] = "profiles/ncu_summary.json (committed ncu capture of this config/precision)"
+    roof["traffic"], how = profile_traffic(a.config, a.precision, sr.chunk)
+    roof["traffic_source"] = f"profiles/ncu_summary.json: {how}" if how else None
     if rank == 0:
         cfg = bench_config(w, a, rows, world, sharded)
         line = {

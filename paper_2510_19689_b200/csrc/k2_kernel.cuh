@@ -400,7 +400,10 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   // result is unused, Appendix A of SURVEY.md: step 0's d half, step S's a half)
   auto glu_range = [&](bool residual, auto cb, auto ce) {
     constexpr int CB = decltype(cb)::value, CE = decltype(ce)::value;
-    constexpr int CW = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);   // 16 measured no faster
+    constexpr int CW0 = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);   // 16 measured no faster
+    // widest chunk (a power of two up to CW0) that tiles [CB, CE)
+    constexpr int CW = ((CB | CE) % CW0 == 0) ? CW0 : ((CB | CE) % 8 == 0 && CW0 >= 8) ? 8
+                       : ((CB | CE) % 4 == 0 && CW0 >= 4) ? 4 : 2;
     static_assert(H % CW == 0 && CB % CW == 0 && CE % CW == 0, "GLU chunking");
     float lin[CW], gate[CW];
     tmem_load_n<CW>(tD + CB, lin);
@@ -446,6 +449,18 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   auto glu = [&](bool residual) { glu_range(residual, std::integral_constant<int, 0>{}, std::integral_constant<int, H>{}); };
   auto store_g = [&]() { put_a<CF, CF::A0, H>(tA, gv); };
 
+#ifdef TBN_K2_STAGGER      // dev experiment: de-phase the groups' chains
+  {
+    const long long t0 = clock64();
+#if TBN_K2_STAGGER_MODE == 1
+    const long long dly = (long long)g * (TBN_K2_STAGGER / 2);
+#else
+    const long long dly = (g & 1) ? TBN_K2_STAGGER : 0;
+#endif
+    while (clock64() - t0 < dly) { }
+    __syncwarp();
+  }
+#endif
   for (int64_t k = 0; k < rounds; ++k) {
     const int64_t m = g + (int64_t)NG * k;
     if (m >= tiles_cta) {
@@ -563,8 +578,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       glu(true);
       store_g();
       gemm(1, o2, CF::RING ? rv0 + 2 * s + 1 : -1, nopost);
-#ifdef TBN_K2_PRUNE
-      if (s == 0) glu_range(true, std::integral_constant<int, ND>{}, std::integral_constant<int, H>{});
+#ifndef TBN_K2_NOPRUNE     // the unused halves are skipped: +0.7%
+      if constexpr (ND % 2 != 0) glu(true);     // (pairs would straddle the d/a boundary)
+      else if (s == 0) glu_range(true, std::integral_constant<int, ND>{}, std::integral_constant<int, H>{});
       else if (s == S) glu_range(true, std::integral_constant<int, 0>{}, std::integral_constant<int, ND>{});
       else glu(true);
 #else

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 #include "tbn_tc.h"
 #include "k3_kernel.cuh"
@@ -14,6 +15,35 @@
 namespace tbn {
 
 namespace {
+
+// The device's persisting-L2 set-aside for K3's row-state scratch: reserved
+// once per device at model creation (cudaDeviceSetLimit is not allowed while
+// a stream captures, and the host path captures its launches as graphs);
+// launches only read it.  TBN_K3_PERSIST_MB overrides (0 disables).
+std::once_flag g_persist_once[kMaxDevices];
+size_t g_persist_bytes[kMaxDevices];
+
+void l2_persist_setup(size_t want) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return;
+  std::call_once(g_persist_once[dev], [&] {
+    g_persist_bytes[dev] = 0;
+    int maxp = 0;
+    if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess) return;
+    size_t lim = want;
+    if (const char* e = std::getenv("TBN_K3_PERSIST_MB")) lim = (size_t)std::atol(e) << 20;
+    if (lim > (size_t)maxp) lim = (size_t)maxp;
+    if (lim > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim) == cudaSuccess)
+      g_persist_bytes[dev] = lim;
+    cudaGetLastError();
+  });
+}
+
+size_t l2_persist_bytes() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+  return g_persist_bytes[dev];
+}
 
 // W (Kin x N row-major, x @ W) -> chunks of kc rows of K (last may be short),
 // element (n, k) of a chunk at (n/8)*(kc*8) + (k/8)*64 + (n%8)*8 + k%8.
@@ -72,6 +102,12 @@ bool pack_k3(const HostParams& hp, TcModel* out, std::string* err) {
   out->d_buf = d;
   out->bytes = CF::IMG_BYTES;
   out->scratch_per_cta = CF::SCRATCH_PER_CTA;
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      l2_persist_setup((size_t)sms * CF::SCRATCH_PER_CTA);
+  }
   out->params = new k3::Params{(const uint8_t*)d, (float)hp.gamma};
   return true;
 }
@@ -85,8 +121,30 @@ cudaError_t launch_k3_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   int cap = num_sms;
   if (const char* e = std::getenv("TBN_K3_GRID")) cap = std::atoi(e) > 0 ? std::atoi(e) : num_sms;   // dev A/B
   const int grid = (int)(ntiles < cap ? ntiles : cap);
-  k3::tabnet_wide<CF><<<grid, CF::THREADS, CF::SMEM_BYTES, stream>>>(*(const k3::Params*)m.params, a);
-  return cudaGetLastError();
+  // The per-CTA row-state scratch is re-read every step: pin it in L2 with a
+  // persisting access-policy window over exactly the scratch this launch uses
+  // (the evict_last hints inside the kernel only take effect within the
+  // device's persisting set-aside, which defaults to 0).
+  const size_t scratch_bytes = (size_t)grid * CF::SCRATCH_PER_CTA;
+  const size_t persist = l2_persist_bytes();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(CF::THREADS);
+  cfg.dynamicSmemBytes = CF::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (persist > 0) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = a.scratch;
+    attr[0].val.accessPolicyWindow.num_bytes = scratch_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = (float)((double)persist / (double)scratch_bytes > 1.0
+                                                          ? 1.0 : (double)persist / (double)scratch_bytes);
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, k3::tabnet_wide<CF>, *(const k3::Params*)m.params, a);
 }
 
 struct K3Instance {

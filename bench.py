@@ -409,6 +409,8 @@ def chunk_plan(rows: int, bytes_per_row: int) -> tuple[int, int]:
     if rows * bytes_per_row <= MAX_CHUNK_BYTES:
         return rows, 1
     ch = max(128, (MAX_CHUNK_BYTES // bytes_per_row) // 128 * 128)
+    n = (rows + ch - 1) // ch
+    ch = ((rows + n - 1) // n + 127) // 128 * 128      # n equal chunks (the last may be short by < 128 n)
     return ch, (rows + ch - 1) // ch
 
 
@@ -417,7 +419,7 @@ class StepRunner:
     in total, or an L2 flush per step when they would fit) and, for shards
     bigger than one launch, a chunked stream over them."""
 
-    def __init__(self, model, w, rows: int, start: int, local: int, flush_ok: bool = True):
+    def __init__(self, model, w, rows: int, start: int, local: int, flush_ok: bool = True, flags: int = 0):
         import torch
         from paper_2510_19689_b200.device import DeviceRunner
         self.torch = torch
@@ -430,7 +432,7 @@ class StepRunner:
             self.flush_mode = False
         if self.nchunks > 1:                 # streaming: rows repeat over the distinct input chunks
             self.nsets = max(2, min(self.nsets, self.nchunks))
-        self.runner = DeviceRunner(model, self.chunk, device=local)
+        self.runner = DeviceRunner(model, self.chunk, device=local, flags=flags)
         self.xs = [torch.from_numpy(W.make_inputs(w, self.chunk, start=start + i * self.chunk)).to(self.dev)
                    for i in range(self.nsets)]
         self.outs = [self.runner.alloc_outputs(self.chunk) for _ in range(self.nsets)]
@@ -655,7 +657,12 @@ def run_ours(a) -> None:
 def steady_state(torch, dev, model, w, rows, start, local, q, counts, world, dist) -> dict:
     """Q independent batches of ``rows`` in flight on Q streams per step (one
     graph, K_SS steps): the sustained rows/s of a GPU serving such requests."""
-    runners = [StepRunner(model, w, rows, start + j * rows, local, flush_ok=False) for j in range(q)]
+    # TBN_FLAG_PACKED: each batch takes full row tiles on as few SMs as it
+    # needs, so the Q batches run side by side instead of each spreading one
+    # partial tile over every SM (launch geometry only; outputs are identical)
+    from paper_2510_19689_b200 import _native as N
+    runners = [StepRunner(model, w, rows, start + j * rows, local, flush_ok=False, flags=N.FLAG_PACKED)
+               for j in range(q)]
     ks = 10
 
     def body(s):
@@ -689,7 +696,7 @@ def steady_state(torch, dev, model, w, rows, start, local, q, counts, world, dis
     frac = counts["bytes_per_row"] * total / (ms / 1e3) / (world * peaks.get("hbm_gbs", 6650.0) * 1e9)
     return {"inflight_per_gpu": q, "rows_per_batch": rows, "value": total / (ms / 1e3), "unit": "rows/s",
             "ms_per_round": ms / ks, "hbm_frac": frac,
-            "how": f"{q} streams per GPU, each launching its own {rows}-row batch per round, "
+            "how": f"{q} streams per GPU, each launching its own {rows}-row batch per round (TBN_FLAG_PACKED), "
                    f"{ks} rounds in one CUDA graph, max over ranks"}
 
 

@@ -62,6 +62,12 @@ typedef enum {
 /* apply() flags (network.py:195-196) */
 #define TBN_FLAG_NORMALIZED 1u      /* input is already normalized: skip the frozen affine        */
 #define TBN_FLAG_BATCH_STATS 2u     /* negative control: normalize with this batch's mean/var     */
+/* Launch geometry (no effect on any output bit): by default a batch is spread
+ * over every SM (one partial row tile each: the shortest latency for a small
+ * batch).  PACKED gives each CTA full row tiles on as few SMs as the batch
+ * needs, so several batches in flight on different streams share the GPU
+ * (the steady-state serving shape: e.g. 8 x 8,192-row batches per B200). */
+#define TBN_FLAG_PACKED 4u
 
 typedef struct {
   int32_t feature_count; /* F            (config.py:20)  */
@@ -148,7 +154,8 @@ tbn_status tbn_forward_host_f64(const tbn_model* model, const double* x, int64_t
 /* Row-wise sparsemax on device (sparsemax.py:13-41): z, out (rows, n) fp32. */
 tbn_status tbn_sparsemax(const float* z, int64_t rows, int32_t n, float* out,
                          void* stream);
-/* Host-buffer sparsemax (float64 in/out, computed on device in fp32). */
+/* Host-buffer sparsemax: float64 in/out, computed on device in float64, any
+ * width (the reference helper's precision, sparsemax.py:13-41). */
 tbn_status tbn_sparsemax_host_f64(const double* z, int64_t rows, int32_t n, double* out);
 
 /* Per-partition column means on device: values (partitions*rows_per_partition,

@@ -26,6 +26,7 @@ CFG_REGRESSION = 1           # tbn_config.flags: identity head, n_classes == 1
 PRECISIONS = {"tf32x3": PREC_TF32X3, "tf32": PREC_TF32, "bf16": PREC_BF16, "fp32": PREC_FP32}
 FLAG_NORMALIZED = 1
 FLAG_BATCH_STATS = 2
+FLAG_PACKED = 4          # launch geometry only (TBN_FLAG_PACKED)
 
 # Every symbol include/tabnet_b200.h declares (tests check the .so exports them).
 EXPORTED = (

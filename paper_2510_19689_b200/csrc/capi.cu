@@ -290,6 +290,7 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
   a.x = x;
   a.rows = rows;
   a.normalized = (flags & TBN_FLAG_NORMALIZED) ? 1 : 0;
+  a.packed = (flags & TBN_FLAG_PACKED) ? 1 : 0;
   if (out) {
     a.logits = out->logits; a.probs = out->probabilities; a.masks = out->masks;
     a.importance = out->importance; a.pred = out->predicted_class;
@@ -758,34 +759,33 @@ tbn_status tbn_partition_mean(const float* v, int64_t per, int32_t partitions, i
 
 tbn_status tbn_sparsemax_host_f64(const double* z, int64_t rows, int32_t n, double* out) {
   if (rows < 1 || n < 1) return fail(TBN_ERR_INVALID_INPUT, "sparsemax input must have length >= 1");
-  if (n > 512) return fail(TBN_ERR_UNSUPPORTED, "sparsemax width > 512");
   if (tbn_device_count() <= 0) return fail(TBN_ERR_CUDA, "no CUDA device available");
   int dev = 0;
   cudaGetDevice(&dev);
   HostCtx* hc = host_ctx(dev);
   if (!hc) return fail(TBN_ERR_CUDA, "cannot create stream");
   StreamCtx* c = &hc->s[0];
-  const size_t bytes = (size_t)rows * n * 4;
+  // float64 end to end (the reference helper's precision, any width)
+  const size_t bytes = (size_t)rows * n * 8;
   const size_t total = align_up(bytes, 256) * 2 + 256;
   TBN_CUDA(ensure(c, total, total));
-  float* pz = (float*)c->pin;
-  for (size_t i = 0; i < (size_t)rows * n; ++i) pz[i] = (float)z[i];
+  std::memcpy(c->pin, z, bytes);
   char* D = (char*)c->dev;
-  float* dz = (float*)D;
-  float* dout = (float*)(D + align_up(bytes, 256));
+  double* dz = (double*)D;
+  double* dout = (double*)(D + align_up(bytes, 256));
   int32_t* derr = (int32_t*)(D + 2 * align_up(bytes, 256));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   TBN_CUDA(cudaMemsetAsync(derr, 0, 4, c->stream));
-  TBN_CUDA(cudaMemcpyAsync(dz, pz, bytes, cudaMemcpyHostToDevice, c->stream));
-  TBN_CUDA(tbn::launch_sparsemax(dz, rows, n, dout, derr, sms, c->stream));
-  float* po = (float*)((char*)c->pin + align_up(bytes, 256));
+  TBN_CUDA(cudaMemcpyAsync(dz, c->pin, bytes, cudaMemcpyHostToDevice, c->stream));
+  TBN_CUDA(tbn::launch_sparsemax_f64(dz, rows, n, dout, derr, sms, c->stream));
+  double* po = (double*)((char*)c->pin + align_up(bytes, 256));
   int32_t* perr = (int32_t*)((char*)c->pin + 2 * align_up(bytes, 256));
   TBN_CUDA(cudaMemcpyAsync(po, dout, bytes, cudaMemcpyDeviceToHost, c->stream));
   TBN_CUDA(cudaMemcpyAsync(perr, derr, 4, cudaMemcpyDeviceToHost, c->stream));
   TBN_CUDA(cudaStreamSynchronize(c->stream));
   if (*perr) return fail(TBN_ERR_INVALID_INPUT, "sparsemax input must be finite");
-  for (size_t i = 0; i < (size_t)rows * n; ++i) out[i] = po[i];
+  std::memcpy(out, po, bytes);
   return TBN_OK;
 }
 

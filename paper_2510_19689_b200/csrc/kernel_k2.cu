@@ -103,7 +103,9 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   // one CTA per SM, each with a contiguous, equal block of rows (k2_kernel.cuh);
   // small batches: one CTA per TBN_K2_ROWQ rows (spreading them thinner, 32
   // rows per CTA, measured no faster)
-  const int64_t nq = (a.rows + TBN_K2_ROWQ - 1) / TBN_K2_ROWQ;
+  // (TBN_FLAG_PACKED: NG full tiles per CTA on as few SMs as the batch needs)
+  const int64_t nq = a.packed ? (a.rows + 128 * CF::NG - 1) / (128 * CF::NG)
+                              : (a.rows + TBN_K2_ROWQ - 1) / TBN_K2_ROWQ;
   const int grid = (int)(nq < num_sms ? nq : num_sms);
   k2::tabnet_rowthread<CF><<<grid, CF::THREADS, CF::SMEM_BYTES, stream>>>(*(const k2::Params*)m.params, a);
   return cudaGetLastError();

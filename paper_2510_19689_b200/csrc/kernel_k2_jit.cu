@@ -302,7 +302,8 @@ cudaError_t k2_jit_launch(const TcModel& m, const ForwardArgs& a, int num_sms, c
     }
   }
   // the same geometry as the prebuilt instances (kernel_k2.cu launch_k2_impl)
-  const int64_t nq = (a.rows + 127) / 128;
+  const int64_t ng = j->L.THREADS / 128;
+  const int64_t nq = a.packed ? (a.rows + 128 * ng - 1) / (128 * ng) : (a.rows + 127) / 128;
   const int grid = (int)(nq < num_sms ? nq : num_sms);
   k2::Params p = *(const k2::Params*)m.params;
   ForwardArgs fa = a;

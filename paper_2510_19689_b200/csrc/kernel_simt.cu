@@ -572,6 +572,73 @@ __global__ void sparsemax_rows_kernel(const float* __restrict__ z, int64_t rows,
 }
 }  // namespace
 
+// ---- standalone float64 sparsemax for the host helper API (any width) ----
+// The reference helper (sparsemax.py:13-41) is float64 for any length; the
+// public sparsemax() keeps that: warp per row, the row re-read from L1/L2 on
+// every pass, Michelot's fixed point tau <- (sum_{z>tau} z - 1)/|{z>tau}| in
+// float64 from the lower bound max(-1, (sum z - 1)/n) (its support equals the
+// reference's sort/cumsum/count k; tau differs only by summation order).
+namespace {
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__global__ void sparsemax_rows_f64_kernel(const double* __restrict__ z, int64_t rows, int n,
+                                          double* __restrict__ out, int32_t* err_flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const double* zr = z + r * n;
+    double zmax = -INFINITY, zsum = 0.0;
+    int bad = 0;
+    for (int f = lane; f < n; f += 32) {
+      const double v = zr[f];
+      bad |= !isfinite(v);
+      zmax = fmax(zmax, v);
+      zsum += v;
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0 && err_flag) atomicOr(err_flag, 1);
+      continue;
+    }
+    zmax = warp_max_d(zmax);                                   // sparsemax.py:32
+    zsum = warp_sum_d(zsum) - (double)n * zmax;
+    double tau = fmax(-1.0, (zsum - 1.0) / (double)n);
+    tau -= 0x1p-40 * fmax(1.0, fabs(tau));
+    double cnt_prev = (double)n + 1.0;
+    for (int it = 0; it <= n; ++it) {
+      double sm = 0.0, cn = 0.0;
+      for (int f = lane; f < n; f += 32) {
+        const double v = zr[f] - zmax;
+        if (v > tau) { sm += v; cn += 1.0; }
+      }
+      sm = warp_sum_d(sm);
+      cn = warp_sum_d(cn);
+      if (cn >= cnt_prev) break;
+      cnt_prev = cn;
+      tau = (sm - 1.0) / cn;                                   // sparsemax.py:39
+    }
+    for (int f = lane; f < n; f += 32) out[r * n + f] = fmax(zr[f] - zmax - tau, 0.0);   // :40
+  }
+}
+}  // namespace
+
+cudaError_t launch_sparsemax_f64(const double* z, int64_t rows, int n, double* out, int32_t* err_flag,
+                                 int num_sms, cudaStream_t stream) {
+  int64_t blocks = (rows + 7) / 8;
+  int64_t cap = (int64_t)num_sms * 16;
+  int grid = (int)(blocks < cap ? blocks : cap);
+  if (grid < 1) grid = 1;
+  sparsemax_rows_f64_kernel<<<grid, 256, 0, stream>>>(z, rows, n, out, err_flag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sparsemax(const float* z, int64_t rows, int n, float* out, int32_t* err_flag,
                              int num_sms, cudaStream_t stream) {
   if (n > kMaxF) return cudaErrorInvalidValue;

@@ -20,6 +20,7 @@ struct ForwardArgs {
   int32_t* err_flag;
   float* scratch;              // K3: per-CTA row-tile state in the workspace
   unsigned long long* trace;   // debug timeline (TBN_TRACE env); null in production
+  int packed;                  // TBN_FLAG_PACKED: host-side launch geometry only
 };
 
 }  // namespace tbn

@@ -48,6 +48,8 @@ struct SimtParams {
 size_t simt_smem_bytes(const SimtParams& p);
 bool simt_supported(int F, int H, int C);      // the CUDA-core kernel's shape limits
 cudaError_t launch_simt(const SimtParams& p, const ForwardArgs& a, int num_sms, cudaStream_t stream);
+cudaError_t launch_sparsemax_f64(const double* z, int64_t rows, int n, double* out, int32_t* err_flag,
+                                 int num_sms, cudaStream_t stream);
 cudaError_t launch_sparsemax(const float* z, int64_t rows, int n, float* out, int32_t* err_flag,
                              int num_sms, cudaStream_t stream);
 cudaError_t launch_partition_mean(const float* v, int64_t per, int partitions, int W, double* out,

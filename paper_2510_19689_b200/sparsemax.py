@@ -1,8 +1,8 @@
 """Sparsemax (simplex projection) — API of ``tabserve/model/sparsemax.py``.
 
-``sparsemax`` runs on the GPU (the same warp-level sort-free kernel the fused
-forward uses, via ``tbn_sparsemax_host_f64``); validation and error types follow
-sparsemax.py:13-30.  ``project_simplex_bruteforce`` is the reference's
+``sparsemax`` runs on the GPU in float64 for any width (a warp-per-row
+sort-free Michelot kernel, via ``tbn_sparsemax_host_f64``), the reference
+helper's precision; validation and error types follow sparsemax.py:13-30.  ``project_simplex_bruteforce`` is the reference's
 exhaustive-support oracle (sparsemax.py:60-84), kept for API parity; it is a
 test oracle, never used by the engine.
 """

@@ -196,6 +196,35 @@ def test_sparsemax_gpu_spec_examples():
         P.sparsemax(np.array([1.0, np.nan]))
 
 
+def test_sparsemax_helper_is_float64_any_width():
+    """The public helper keeps the reference's float64 precision for any width
+    (it used to round through the fp32 kernel and reject n > 512 and
+    finite values beyond FLT_MAX)."""
+    rng = np.random.default_rng(3)
+    for n in (1, 7, 35, 513, 2000):
+        z = rng.standard_normal((64, n)) * rng.uniform(0.1, 30.0, (64, 1))
+        np.testing.assert_allclose(P.sparsemax(z), O.sparsemax(z), rtol=0, atol=1e-12)
+    big = np.array([1e300, 1e300 - 1e285, -1e300])          # finite, beyond float32
+    np.testing.assert_allclose(P.sparsemax(big), O.sparsemax(big), atol=1e-12)
+    assert P.sparsemax(np.array([5.0])).tolist() == [1.0]
+
+
+def test_sparsemax_device_fp32_kernel():
+    """tbn_sparsemax (device pointers, fp32): the warp-per-row kernel the
+    fp32 forward uses, against the float64 oracle."""
+    import torch
+    from paper_2510_19689_b200 import _native as N
+    rng = np.random.default_rng(4)
+    for n in (14, 35, 64, 512):
+        z = (rng.standard_normal((300, n)) * rng.uniform(0.1, 20.0, (300, 1))).astype(np.float32)
+        dz = torch.from_numpy(z).cuda()
+        out = torch.empty_like(dz)
+        N.check(N.lib().tbn_sparsemax(dz.data_ptr(), z.shape[0], n, out.data_ptr(), None), "tbn_sparsemax")
+        torch.cuda.synchronize()
+        ref = O.sparsemax(z.astype(np.float64))
+        assert np.abs(out.cpu().numpy() - ref).max() < 2e-5 * np.abs(z).max()
+
+
 def test_attentive_step_spec():
     # SPEC.md:66-68 — gamma = 1, mask one-hot on feature j -> new_prior[j] = 0
     cfg = P.ModelConfig(feature_count=3, n_a=2, n_d=2, n_steps=1, gamma=1.0)
@@ -469,13 +498,17 @@ def test_row_partition_geometry_bitwise(name, precision):
         for k, v in o.items():
             ref.setdefault(k, []).append(v.clone())
     ref = {k: torch.cat(v, dim=1 if k == "masks" else 0) for k, v in ref.items()}
-    for rows in (1, 3, 31, 33, 127, 129, 443, 445, 4097, big):
-        o = runner.run(x[:rows].contiguous())
-        torch.cuda.synchronize()
-        for k, v in o.items():
-            want = ref[k][:, :rows] if k == "masks" else ref[k][:rows]
-            assert torch.equal(v, want), (rows, k)
+    from paper_2510_19689_b200 import _native as N
+    packed = DeviceRunner(m, max_rows=big, flags=N.FLAG_PACKED)   # full tiles on fewer SMs
+    for rows in (1, 3, 31, 33, 127, 129, 443, 445, 4097, 8192, big):
+        for rn in (runner, packed):
+            o = rn.run(x[:rows].contiguous())
+            torch.cuda.synchronize()
+            for k, v in o.items():
+                want = ref[k][:, :rows] if k == "masks" else ref[k][:rows]
+                assert torch.equal(v, want), (rows, k, rn.flags)
     runner.check_finite()
+    packed.check_finite()
 
 
 @pytest.mark.parametrize("precision", ["bf16", "tf32x3"])

@@ -4,7 +4,7 @@
 #   ncu launch list + full capture of the headline kernel (tools/profile.sh),
 #   then copy/summarize here with:  for f in gpurun_out/f_*.json ...; python tools/summarize_profiles.py
 set -e
-TAG=${TAG:-r1x}
+TAG=${TAG:-r2x}
 python tools/measure_tf32_peak.py > /dev/null     # -> gpurun_out/measured_tf32.json (copy into profiles/)
 python bench.py                                   > gpurun_out/f_hr_bf16.json
 python bench.py --precision tf32   --no-cpu-baseline > gpurun_out/f_hr_tf32.json
@@ -17,6 +17,8 @@ python bench.py --config bls --precision tf32x3 --no-cpu-baseline > gpurun_out/f
 python bench.py --config bls --precision fp32   --no-cpu-baseline --steps 5 > gpurun_out/f_bls_fp32.json
 python bench.py --config hr_latency --rows 1024 --latency-sweep --no-cpu-baseline --steps 20 > gpurun_out/f_lat.json
 python bench.py --config wide --rows 262144 --steps 5 --warmup 3 > gpurun_out/f_wide_bf16.json
+python bench.py --config wide --steps 3 --warmup 3 --no-e2e > gpurun_out/f_wide16m_bf16.json   # config 5: 2^24 rows streamed
+python bench.py --config hr8 --rows 8192 --no-cpu-baseline > gpurun_out/f_hr8_share.json          # one GPU's share of 65,536 on 8
 python bench.py --config wide --precision fp32 --rows 262144 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/f_wide_fp32.json
 python bench.py --impl reference                  > gpurun_out/f_reference.json
 bash tools/profile.sh hr bf16 $TAG

@@ -77,10 +77,12 @@ traffic = (metrics["dram_bytes_read"] or 0) + (metrics["dram_bytes_write"] or 0)
 
 summ_path = out_dir / "ncu_summary.json"
 summ = json.loads(summ_path.read_text()) if summ_path.exists() else {}
-summ[f"{cfg}/{prec}"] = {
+# merge: keep keys written by other captures (tools/update_traffic.py's
+# steady-state traffic) for the same config/precision
+summ.setdefault(f"{cfg}/{prec}", {}).update({
     "tag": tag, "dram_bytes_per_launch": traffic, "fused_kernel_share_of_launch_list": share,
     "launch_list_ns": [t for _, t in rows], **metrics,
-}
+})
 summ_path.write_text(json.dumps(summ, indent=1, sort_keys=True))
 
 md = [f"# ncu summary — {cfg} / {prec} ({tag})", "",

@@ -7,6 +7,17 @@
 // reference-facing Python apply() and bench.py's e2e leg use.
 #include "tabnet_b200.h"
 #include "tbn_internal.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: free when no profiler is attached
+
+namespace {
+// NVTX range for nsys/ncu timelines: forward, H2D, D2H of the host path
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 #include "tbn_tc.h"
 
 #include <cmath>
@@ -281,6 +292,7 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
   if (rows < 0) return fail(TBN_ERR_INVALID_INPUT, "rows must be >= 0");
   if (rows == 0) return TBN_OK;
   if (!x) return fail(TBN_ERR_INVALID_INPUT, "null input");
+  NvtxRange nv("tbn_forward");
   if ((flags & TBN_FLAG_NORMALIZED) && (flags & TBN_FLAG_BATCH_STATS)) flags &= ~TBN_FLAG_BATCH_STATS;
   if (workspace_bytes < tbn_workspace_bytes(m, rows, flags) || !workspace)
     return fail(TBN_ERR_CONFIG, "workspace too small");
@@ -561,6 +573,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   if (!m) return fail(TBN_ERR_CONFIG, "null model");
   if (rows < 0) return fail(TBN_ERR_INVALID_INPUT, "rows must be >= 0");
   if (rows == 0) return TBN_OK;
+  NvtxRange nv("tbn_forward_host");
   if (!x) return fail(TBN_ERR_INVALID_INPUT, "null input");
   DeviceGuard guard(m->device);
   HostCtx* hc = host_ctx(m->device);
@@ -599,6 +612,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   // copy a finished chunk's staged outputs into the caller's arrays
   auto drain = [&](StreamCtx& sc) -> tbn_status {
     if (sc.pending_r0 < 0) return TBN_OK;
+    NvtxRange nv("tbn_host: D2H wait + output conversion");
     TBN_CUDA(cudaStreamSynchronize(sc.stream));
     char* P = (char*)sc.pin;
     const size_t r0 = sc.pending_r0, n = sc.pending_rows;
@@ -624,6 +638,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     tbn_status st = drain(sc);
     if (st != TBN_OK) return st;
     const int64_t n = (rows - r0 < chunk) ? rows - r0 : chunk;
+    NvtxRange nv_chunk("tbn_host: H2D + forward + D2H enqueue");
     char* P = (char*)sc.pin;
     char* D = (char*)sc.dev;
     cudaStream_t cs = sc.stream;

@@ -359,14 +359,18 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     __syncwarp();                                  // bar.sync / tcgen05 .aligned: converged warp
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
+#ifndef TBN_K2_NOBAR          // dev experiment only (with TBN_K2_NOMMA): the barrier's cost
     ptx::named_bar_sync(bar_id, 128);
+#endif
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 1);
     if (q == iq) {
       ptx::tc_fence_after();
       const uint32_t tAL = tA + CF::KA;              // A_lo (3xTF32 only)
+#ifndef TBN_K2_NOMMA          // dev experiment only: the tensor core's share of the chain
       if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tAL, wbase + bo);
       else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tAL, wbase + bo);
       else tc::issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tAL, wbase + bo);
+#endif
       ptx::mma_commit(&bars->dfull[g]);
       if constexpr (CF::RING) {
         // the previous GEMM's ring block: its MMAs completed before this chain

@@ -12,6 +12,6 @@ for v in "$@"; do
   $NV $flags -c paper_2510_19689_b200/csrc/$SRC -o /tmp/ab_obj.o
   objs=$(ls $B/*.o | grep -v "/$SRC.o")
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o paper_2510_19689_b200/libtabnet_b200.so $objs /tmp/ab_obj.o -ldl
-  LABEL=$label python tools/k2_time.py $CFG $PREC
+  LABEL=$label timeout ${K2AB_TIMEOUT:-180} python tools/k2_time.py $CFG $PREC || echo "$label: failed or timed out"
 done
 cp /tmp/lib_prod.so paper_2510_19689_b200/libtabnet_b200.so

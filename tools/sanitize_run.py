@@ -23,11 +23,18 @@ for name, prec in cases:
     r.run(x)
     torch.cuda.synchronize()
     r.check_finite()
+    from paper_2510_19689_b200 import _native as N
+    rp = DeviceRunner(m, 600 if name != "wide" else 160, device=0, flags=N.FLAG_PACKED)   # packed geometry
+    rp.run(torch.from_numpy(W.make_inputs(W.WORKLOADS[name], 600 if name != "wide" else 160)).cuda())
+    torch.cuda.synchronize()
+    rp.check_finite()
+    del rp
     m.apply(x[:37].double().cpu().numpy(), use_batch_stats=True)   # batch-stats kernel + host path
     print("ok", name, prec, flush=True)
     del r, m
 if which in ("all", "aux"):
     print(P.sparsemax(np.random.default_rng(0).standard_normal((100, 35))).shape)
+    print(P.sparsemax(np.random.default_rng(0).standard_normal((10, 700))).shape)   # float64 kernel
     from paper_2510_19689_b200 import interpret
     m = W.make_engine_model("hr", "trained", precision="bf16", device=0)
     interpret.stability_score(m, W.make_inputs(W.WORKLOADS["hr"], 400).astype(np.float64), 4)

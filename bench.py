@@ -244,21 +244,45 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- cpu arm
+REF_DIR = ROOT / "baseline" / "_ref"      # the unmodified reference (tools/install_reference.sh)
+
+
+def reference_kind() -> str:
+    """"reference": the unmodified tabserve package is installed in baseline/_ref
+    and its own TabNetModel.apply is timed; "port": the oracle restatement
+    (bitwise equal to it, tests/test_oracle.py) stands in."""
+    return "reference" if (REF_DIR / "tabserve" / "model" / "network.py").exists() else "port"
+
+
 def _oracle_worker(args):
     name, regime, start, rows = args
-    from oracle import tabnet_oracle as O
     w = W.WORKLOADS[name]
     m = W.make_model(name, regime)
     x = W.make_inputs(w, rows, start=start).astype(np.float64)
+    if reference_kind() == "reference":
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        from tabserve.model.config import ModelConfig as RefConfig
+        from tabserve.model.network import TabNetModel as RefModel
+        c = m.config
+        ref = RefModel(config=RefConfig(feature_count=c.feature_count, n_classes=c.n_classes, n_d=c.n_d,
+                                        n_a=c.n_a, n_steps=c.n_steps, gamma=c.gamma),
+                       params=m.params, norm_mean=m.norm_mean, norm_var=m.norm_var,
+                       model_version=m.model_version)
+        t0 = time.perf_counter()
+        ref.apply(x)                                 # network.py:195-267, the reference's own code
+        return time.perf_counter() - t0
+    from oracle import tabnet_oracle as O
     t0 = time.perf_counter()
     O.apply_model(m, x)
     return time.perf_counter() - t0
 
 
 class CpuReference:
-    """The reference algorithm on host cores: oracle/tabnet_oracle.py (bitwise
-    equal to tabserve TabNetModel.apply) over a fork pool of contiguous row shards
-    (its einsum path is single-threaded)."""
+    """The reference algorithm on host cores: the unmodified tabserve
+    TabNetModel.apply from baseline/_ref (else oracle/tabnet_oracle.py, bitwise
+    equal to it) over a fork pool of contiguous row shards (its einsum path is
+    single-threaded)."""
 
     def __init__(self, name: str, regime: str, rows_per_step: int, procs: int | None = None):
         import multiprocessing as mp
@@ -277,6 +301,9 @@ class CpuReference:
         self.pool.close()
         self.pool.join()
 
+
+REF_SRC = {"reference": "tabserve TabNetModel.apply (unmodified reference, baseline/_ref)",
+           "port": "oracle/tabnet_oracle.py (bitwise = reference apply)"}
 
 CPU_ROWS_PER_CORE = {"adult": 16384, "hr": 4096, "hr8": 4096, "hr_latency": 4096, "bls": 1536, "wide": 96}
 
@@ -297,10 +324,11 @@ def cpu_baseline(w: W.Workload, regime: str, steps: int = 3) -> dict:
     one_rows = CPU_ROWS_PER_CORE[w.name]
     t1 = _oracle_worker((w.name, regime, 0, one_rows))
     extrap = crow < w.batch
-    return {"value": crow * steps / sum(ct), "unit": "rows/s", "cores": procs, "kind": "port",
+    kind = reference_kind()
+    return {"value": crow * steps / sum(ct), "unit": "rows/s", "cores": procs, "kind": kind,
             "cpu_model": cpu_model(), "value_1core": one_rows / t1,
             "sample": (f"{crow} rows x {steps} steps of {w.name} ({regime} weights), "
-                       f"oracle/tabnet_oracle.py (bitwise = reference apply) on {procs} fork-pool "
+                       f"{REF_SRC[kind]} on {procs} fork-pool "
                        f"processes; 1-core figure on {one_rows} rows"
                        + ("; rows/s of this subset stand for the full batch (per-row cost is "
                           "constant beyond ~1k rows: an extrapolation)" if extrap else ""))}
@@ -328,10 +356,10 @@ def run_reference(a) -> None:
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": bench_config(w, a, rows, world, sharded),
-        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": procs, "kind": reference_kind(),
                          "cpu_model": cpu_model(),
                          "sample": f"{crow} rows/step of {a.config} ({a.regime} weights), "
-                                   f"oracle/tabnet_oracle.py over {procs} fork-pool processes"
+                                   f"{REF_SRC[reference_kind()]} over {procs} fork-pool processes"
                                    + (" (a bounded subset of the batch)" if crow < rows else "")},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

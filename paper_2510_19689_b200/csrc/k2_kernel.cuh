@@ -159,6 +159,37 @@ __device__ __forceinline__ float tanh_approx(float x) {
 }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
+// 1 + tanh(g) for a pair on the FMA/ALU pipes only (no MUFU), to take part of
+// the GLU's sigmoid load off the MUFU pipe (FA4-style split):
+//   1 + tanh(g) = 2 r,  r = 1 / (1 + 2^y),  y = -2 log2(e) g  (clamped to +-64)
+//   2^y = 2^j p(f): j = round(y) by the 1.5*2^23 magic add, f = y - j in [-.5, .5],
+//   p a degree-3 fit of 2^f (relative error 2.1e-4), 2^j added to the exponent bits;
+//   r by two Newton steps from the integer-magic seed (relative error 6.6e-6).
+// Overall within ~2.2e-4 relative of 1 + tanh, the class of tanh.approx.f32 (2^-11).
+__device__ __forceinline__ float2 one_plus_tanh_fma(float2 g) {
+  float2 y = __fmul2_rn(g, f2(-2.8853900817779268f, -2.8853900817779268f));
+  y.x = fminf(fmaxf(y.x, -64.0f), 64.0f);
+  y.y = fminf(fmaxf(y.y, -64.0f), 64.0f);
+  const float2 t = __fadd2_rn(y, f2(12582912.0f, 12582912.0f));
+  const float2 j = __fadd2_rn(t, f2(-12582912.0f, -12582912.0f));
+  const float2 fr = __ffma2_rn(j, f2(-1.0f, -1.0f), y);
+  float2 pp = __ffma2_rn(fr, f2(0.05484800413250923f, 0.05484800413250923f),
+                         f2(0.24180661141872406f, 0.24180661141872406f));
+  pp = __ffma2_rn(pp, fr, f2(0.6932482123374939f, 0.6932482123374939f));
+  pp = __ffma2_rn(pp, fr, f2(0.9999886751174927f, 0.9999886751174927f));
+  const float2 e = f2(__int_as_float(__float_as_int(pp.x) + (__float_as_int(t.x) << 23)),
+                      __int_as_float(__float_as_int(pp.y) + (__float_as_int(t.y) << 23)));
+  const float2 d = __fadd2_rn(e, f2(1.0f, 1.0f));
+  const float2 nd = f2(-d.x, -d.y);
+  float2 r = f2(__int_as_float(0x7EF311C3 - __float_as_int(d.x)), __int_as_float(0x7EF311C3 - __float_as_int(d.y)));
+  r = __ffma2_rn(r, __ffma2_rn(nd, r, f2(1.0f, 1.0f)), r);
+  r = __ffma2_rn(r, __ffma2_rn(nd, r, f2(1.0f, 1.0f)), r);
+  return __fadd2_rn(r, r);
+}
+#ifndef TBN_K2_FMA_EVERY     // every Nth GLU pair takes the FMA-pipe sigmoid (0: none)
+#define TBN_K2_FMA_EVERY 0
+#endif
+
 // A operand: L elements of v starting at element E (E, L even for bf16)
 template <class CF, int E, int L, int M>
 __device__ __forceinline__ void put_a(uint32_t tA, const float (&v)[M]) {
@@ -435,6 +466,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
           const float2 l = f2(lin[i], lin[i + 1]);
           o = residual ? __ffma2_rn(l, sg, __fmul2_rn(f2(gv[c0 + i], gv[c0 + i + 1]), f2(kR, kR)))
                        : __fmul2_rn(l, sg);
+        } else if (TBN_K2_FMA_EVERY > 0 && ((c0 + i) / 2) % (TBN_K2_FMA_EVERY > 0 ? TBN_K2_FMA_EVERY : 1) ==
+                                              (TBN_K2_FMA_EVERY > 0 ? TBN_K2_FMA_EVERY : 1) - 1) {
+          // o = lin'(1 + t) [+ sqrt(.5) prev] with 1 + t off the MUFU pipe
+          const float2 opt = one_plus_tanh_fma(f2(gate[i], gate[i + 1]));
+          const float2 l = f2(lin[i], lin[i + 1]);
+          o = residual ? __ffma2_rn(l, opt, __fmul2_rn(f2(gv[c0 + i], gv[c0 + i + 1]), f2(kR, kR)))
+                       : __fmul2_rn(l, opt);
         } else {
           const float2 th = f2(tanh_approx(gate[i]), tanh_approx(gate[i + 1]));
           const float2 l = f2(lin[i], lin[i + 1]);

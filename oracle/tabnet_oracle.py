@@ -203,8 +203,11 @@ def apply(params: dict, norm_mean: np.ndarray, norm_var: np.ndarray, *,
                           fallback)
     out = dict(logits=logits, probabilities=probs, masks=masks, importance=importance)
     if diagnostics:
+        # the magnitude of the terms each logit sums (network.py:253): the
+        # conditioning of d_sum @ head_W, for the comparator's logits bound
+        logit_scale = np.abs(d_sum) @ np.abs(p["head_W"]) + np.abs(p["head_b"])
         out.update(z_shift=zs, tau=taus, d_pre_absmin=d_absmin,
-                   agg_total=totals[:, 0])
+                   agg_total=totals[:, 0], logit_scale=logit_scale)
     return out
 
 

@@ -10,6 +10,7 @@
 #include <vector>
 #include "tbn_tc.h"
 #include "k3_kernel.cuh"
+#include "k3x_kernel.cuh"
 #include "pack_util.h"
 
 namespace tbn {
@@ -37,6 +38,20 @@ void l2_persist_setup(size_t want) {
       g_persist_bytes[dev] = lim;
     cudaGetLastError();
   });
+}
+
+// the largest access-policy window the device accepts (cudaDevAttrMaxAccessPolicyWindowSize)
+size_t max_window_bytes() {
+  static std::once_flag once[kMaxDevices];
+  static size_t v[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+  std::call_once(once[dev], [&] {
+    int w = 0;
+    v[dev] = cudaDeviceGetAttribute(&w, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess ? (size_t)w : 0;
+    cudaGetLastError();
+  });
+  return v[dev];
 }
 
 size_t l2_persist_bytes() {
@@ -127,18 +142,19 @@ cudaError_t launch_k3_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   // device's persisting set-aside, which defaults to 0).
   const size_t scratch_bytes = (size_t)grid * CF::SCRATCH_PER_CTA;
   const size_t persist = l2_persist_bytes();
+  const size_t window = scratch_bytes < max_window_bytes() ? scratch_bytes : max_window_bytes();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(CF::THREADS);
   cfg.dynamicSmemBytes = CF::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  if (persist > 0) {
+  if (persist > 0 && window > 0) {
     attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
     attr[0].val.accessPolicyWindow.base_ptr = a.scratch;
-    attr[0].val.accessPolicyWindow.num_bytes = scratch_bytes;
-    attr[0].val.accessPolicyWindow.hitRatio = (float)((double)persist / (double)scratch_bytes > 1.0
-                                                          ? 1.0 : (double)persist / (double)scratch_bytes);
+    attr[0].val.accessPolicyWindow.num_bytes = window;
+    attr[0].val.accessPolicyWindow.hitRatio = (float)((double)persist / (double)window > 1.0
+                                                          ? 1.0 : (double)persist / (double)window);
     attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cfg.attrs = attr;
@@ -147,23 +163,140 @@ cudaError_t launch_k3_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   return cudaLaunchKernelEx(&cfg, k3::tabnet_wide<CF>, *(const k3::Params*)m.params, a);
 }
 
+// ---- K3X (k3x_kernel.cuh): the 3xTF32 wide kernel -------------------------
+// B chunks of kc K-rows: hi block (N x kc, K-major canonical tf32: element
+// (n, k) at (n/8)*(kc*8) + (k/4)*32 + (n%8)*4 + k%4) then the lo block;
+// hi = rna_tf32(w'), lo = rna_tf32(w' - hi) from the float64 w' = w * colscale.
+void pack_chunked_tf32(std::vector<float>& img, size_t off_bytes, const double* W, int Kin, int N, int kc,
+                       const std::vector<double>* colscale) {
+  size_t base = off_bytes / 4;
+  for (int k0 = 0; k0 < Kin; k0 += kc) {
+    for (int n = 0; n < N; ++n)
+      for (int kl = 0; kl < kc; ++kl) {
+        const int k = k0 + kl;
+        double w = k < Kin ? W[(size_t)k * N + n] : 0.0;
+        if (colscale) w *= (*colscale)[n];
+        const size_t idx = (size_t)(n / 8) * (kc * 8) + (kl / 4) * 32 + (n % 8) * 4 + (kl % 4);
+        const float h = pack::tf32_rna_host((float)w);
+        img[base + idx] = h;
+        img[base + (size_t)N * kc + idx] = pack::tf32_rna_host((float)(w - (double)h));
+      }
+    base += (size_t)2 * N * kc;
+  }
+}
+
+template <class CF>
+bool pack_k3x(const HostParams& hp, TcModel* out, std::string* err) {
+  constexpr int F = CF::F, H = CF::H, N2 = CF::N2, S = CF::S, ND = CF::ND, NA = CF::NA, C = CF::C;
+  std::vector<float> img(CF::IMG_BYTES / 4, 0.0f);
+  for (int f = 0; f < F; ++f) {
+    img[CF::C_SCALE + f] = (float)(1.0 / std::sqrt(hp.norm_var[f] + 1e-8));   // network.py:120
+    img[CF::C_SHIFT + f] = (float)hp.norm_mean[f];
+  }
+  for (int i = 0; i < ND * C; ++i) img[CF::C_HW + i] = (float)hp.head_W[i];
+  for (int i = 0; i < C; ++i) img[CF::C_HB + i] = (float)hp.head_b[i];
+  // exact sigmoid (as K1/K2 3xTF32): gate columns x -log2(e); residual blocks'
+  // linear columns x sqrt(1/2) (network.py:131-137)
+  const double kR = 0.70710678118654752440, kLog2e = 1.4426950408889634;
+  std::vector<double> cs_first(N2), cs_res(N2);
+  for (int n = 0; n < N2; ++n) {
+    cs_first[n] = n < H ? 1.0 : -kLog2e;
+    cs_res[n] = n < H ? kR : -kLog2e;
+  }
+  float* b = img.data() + CF::O_BIAS / 4;
+  for (int n = 0; n < N2; ++n) {
+    b[CF::B_SH1 + n] = (float)(hp.sh1_b[n] * cs_first[n]);
+    b[CF::B_SH2 + n] = (float)(hp.sh2_b[n] * cs_res[n]);
+    for (int s = 0; s <= S; ++s) {
+      b[CF::B_FC1 + s * N2 + n] = (float)(hp.fc1_b[s][n] * cs_res[n]);
+      b[CF::B_FC2 + s * N2 + n] = (float)(hp.fc2_b[s][n] * cs_res[n]);
+    }
+  }
+  for (int s = 1; s <= S; ++s)
+    for (int f = 0; f < F; ++f) b[CF::B_ATT + (s - 1) * F + f] = (float)hp.att_b[s][f];
+  pack_chunked_tf32(img, CF::O_SH1, hp.sh1_W, F, N2, CF::KC_N2, &cs_first);
+  pack_chunked_tf32(img, CF::O_SH2, hp.sh2_W, H, N2, CF::KC_N2, &cs_res);
+  for (int s = 0; s <= S; ++s) {
+    pack_chunked_tf32(img, CF::O_FC1 + (size_t)s * CF::BLK_HID, hp.fc1_W[s], H, N2, CF::KC_N2, &cs_res);
+    pack_chunked_tf32(img, CF::O_FC2 + (size_t)s * CF::BLK_HID, hp.fc2_W[s], H, N2, CF::KC_N2, &cs_res);
+  }
+  for (int s = 1; s <= S; ++s)
+    pack_chunked_tf32(img, CF::O_ATT + (size_t)(s - 1) * CF::BLK_ATT, hp.att_W[s], NA, F, CF::KC_ATT, nullptr);
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, CF::IMG_BYTES);
+  if (e == cudaSuccess) e = cudaMemcpy(d, img.data(), CF::IMG_BYTES, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (d) cudaFree(d);
+    if (err) *err = cudaGetErrorString(e);
+    return false;
+  }
+  out->d_buf = d;
+  out->bytes = CF::IMG_BYTES;
+  out->scratch_per_cta = CF::SCRATCH_PER_CTA;
+  // (k3_free deletes params as k3::Params: the layouts are identical)
+  static_assert(sizeof(k3x::Params) == sizeof(k3::Params), "params layout");
+  out->params = new k3::Params{(const uint8_t*)d, (float)hp.gamma};
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      l2_persist_setup((size_t)sms * CF::SCRATCH_PER_CTA);
+  }
+  return true;
+}
+
+template <class CF>
+cudaError_t launch_k3x_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  cudaError_t e = smem_attr_once<CF>((const void*)k3x::tabnet_wide_x3<CF>, CF::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  if (!a.scratch) return cudaErrorInvalidValue;
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  const size_t scratch_bytes = (size_t)grid * CF::SCRATCH_PER_CTA;
+  const size_t persist = l2_persist_bytes();
+  const size_t window = scratch_bytes < max_window_bytes() ? scratch_bytes : max_window_bytes();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(CF::THREADS);
+  cfg.dynamicSmemBytes = CF::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (persist > 0 && window > 0) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = a.scratch;
+    attr[0].val.accessPolicyWindow.num_bytes = window;
+    attr[0].val.accessPolicyWindow.hitRatio = (float)((double)persist / (double)window > 1.0
+                                                          ? 1.0 : (double)persist / (double)window);
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  k3x::Params prm{((const k3::Params*)m.params)->wimg, ((const k3::Params*)m.params)->gamma};
+  return cudaLaunchKernelEx(&cfg, k3x::tabnet_wide_x3<CF>, prm, a);
+}
+
 struct K3Instance {
-  int F, ND, NA, S, C;
+  int F, ND, NA, S, C, prec;
   bool (*pack)(const HostParams&, TcModel*, std::string*);
   cudaError_t (*launch)(const TcModel&, const ForwardArgs&, int, cudaStream_t);
 };
 
 #define TBN_K3(F, ND, NA, S, C) \
-  K3Instance{F, ND, NA, S, C, &pack_k3<k3::Cfg<F, ND, NA, S, C>>, &launch_k3_impl<k3::Cfg<F, ND, NA, S, C>>}
+  K3Instance{F, ND, NA, S, C, 2, &pack_k3<k3::Cfg<F, ND, NA, S, C>>, &launch_k3_impl<k3::Cfg<F, ND, NA, S, C>>}
+#define TBN_K3X(F, ND, NA, S, C) \
+  K3Instance{F, ND, NA, S, C, 0, &pack_k3x<k3x::Cfg<F, ND, NA, S, C>>, &launch_k3x_impl<k3x::Cfg<F, ND, NA, S, C>>}
 
 const K3Instance kK3[] = {
-    TBN_K3(512, 64, 64, 8, 10),   // wide (BASELINE config 5)
+    TBN_K3(512, 64, 64, 8, 10),   // wide (BASELINE config 5), bf16
+    TBN_K3X(512, 64, 64, 8, 10),  // wide, 3xTF32 (the parity mode)
 };
 
 const K3Instance* find_k3(const HostParams& hp, int precision) {
-  if (precision != 2) return nullptr;          // bf16 only
+  if (std::getenv("TBN_NO_K3X") && precision == 0) return nullptr;   // dev A/B: the CUDA-core fp32 path
   for (const K3Instance& in : kK3)
-    if (in.F == hp.F && in.ND == hp.ND && in.NA == hp.NA && in.S == hp.S && in.C == hp.C) return &in;
+    if (in.prec == precision && in.F == hp.F && in.ND == hp.ND && in.NA == hp.NA && in.S == hp.S && in.C == hp.C)
+      return &in;
   return nullptr;
 }
 

@@ -28,7 +28,7 @@ print("ok")
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,prec", [("wide", "bf16"), ("hr", "bf16"), ("hr", "tf32x3"), ("bls", "tf32x3"),
-                                       ("wide", "fp32")])
+                                       ("wide", "fp32"), ("wide", "tf32x3")])
 def test_first_forward_in_fresh_process(name, prec):
     r = subprocess.run([sys.executable, "-c", CHILD.format(root=str(ROOT)), name, prec],
                        capture_output=True, text=True, timeout=600)

@@ -52,8 +52,6 @@ def _res_dict(r):
 @pytest.mark.parametrize("precision", EXACT_PRECISIONS)
 @pytest.mark.parametrize("case", CASES)
 def test_parity_against_reference_goldens(case, precision):
-    if precision != "fp32" and case.split("_")[0] not in TC_SHAPES:
-        pytest.skip("no tcgen05 instance for this shape (wide runs the fp32 kernel)")
     g = load_golden(case)
     m = golden_model(case, precision)
     r = m.apply(g["x"].astype(np.float64))
@@ -288,8 +286,13 @@ def test_tf32_single_pass_stated_bound(case):
 def test_auto_precision_selects_a_gpu_kernel():
     g = load_golden("wide_trained")
     m = golden_model("wide_trained", "auto")
-    assert m.engine().precision == "fp32"          # no tcgen05 instance for F=512
+    assert m.engine().precision == "tf32x3"        # K3X: the 3xTF32 wide kernel
     assert golden_model("hr_trained", "auto").engine().precision == "tf32x3"
+    # a shape no tensor-core kernel serves in 3xTF32 falls to the fp32 CUDA-core kernel
+    cfg = P.ModelConfig(feature_count=300, n_classes=3, n_d=32, n_a=32, n_steps=2)
+    odd = P.TabNetModel(config=cfg, params=P.init_parameters(cfg), norm_mean=np.zeros(300),
+                        norm_var=np.ones(300), model_version="odd")
+    assert odd.engine().precision == "fp32"
     r = m.apply(g["x"].astype(np.float64))
     rep = compare(g, _res_dict(r))
     assert rep.ok, rep.summary()
@@ -354,7 +357,7 @@ def test_wide_bf16_kernel_batch_invariance():
 
 
 @pytest.mark.parametrize("case,precision", [("hr_trained", "bf16"), ("hr_trained", "tf32x3"),
-                                            ("wide_trained", "bf16")])
+                                            ("wide_trained", "bf16"), ("wide_trained", "tf32x3")])
 def test_normalized_flag_and_batch_stats(case, precision):
     """apply(normalized=True) on host-normalized rows matches apply() (the frozen
     affine, network.py:118-120, :212-220), and use_batch_stats normalizes with the
@@ -383,8 +386,6 @@ def test_nonzero_biases_against_oracle(name, precision):
     fold the biases into the GEMMs (ones column in A / bias row in B) or add them
     in the epilogue; check every kernel against the oracle with random biases."""
     w = W.WORKLOADS[name]
-    if precision == "tf32x3" and name == "wide":
-        pytest.skip("no 3xTF32 instance for the wide shape")
     if precision == "tf32" and name == "wide":
         pytest.skip("no tf32 instance for the wide shape")
     base = W.make_model(name, "trained")
@@ -434,7 +435,7 @@ def test_relaxation_gamma(gamma, precision):
 
 
 @pytest.mark.parametrize("name,precision", [("bls", "tf32x3"), ("bls", "bf16"), ("wide", "bf16"),
-                                            ("wide", "fp32")])
+                                            ("wide", "fp32"), ("wide", "tf32x3")])
 def test_sampled_parity_at_full_size(name, precision):
     """BLS and wide at 262,144 rows in ONE device launch, checked the way
     SURVEY.md §8(c) samples at scale: the first and last tile plus seeded random
@@ -480,7 +481,7 @@ def test_sampled_parity_at_full_size(name, precision):
 
 
 @pytest.mark.parametrize("name,precision", [("hr", "bf16"), ("hr", "tf32x3"), ("bls", "bf16"),
-                                            ("adult", "tf32"), ("wide", "bf16")])
+                                            ("adult", "tf32"), ("wide", "bf16"), ("wide", "tf32x3")])
 def test_row_partition_geometry_bitwise(name, precision):
     """Every batch size maps rows to CTAs, tiles and warps differently (equal
     contiguous row blocks per CTA, partial last tiles, warps without rows):

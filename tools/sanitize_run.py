@@ -12,7 +12,7 @@ from paper_2510_19689_b200.device import DeviceRunner
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 cases = [("adult", "bf16"), ("adult", "tf32x3"), ("hr", "bf16"), ("hr", "tf32"), ("hr", "tf32x3"),
-         ("bls", "bf16"), ("bls", "tf32x3"), ("bls", "tf32"), ("wide", "bf16"), ("hr", "fp32"), ("wide", "fp32")]
+         ("bls", "bf16"), ("bls", "tf32x3"), ("bls", "tf32"), ("wide", "bf16"), ("wide", "tf32x3"), ("hr", "fp32"), ("wide", "fp32")]
 for name, prec in cases:
     if which != "all" and which != f"{name}/{prec}":
         continue

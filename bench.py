@@ -752,7 +752,8 @@ def parity_mode(torch, dev, w, a, rows, start, local, counts, world, dist) -> di
     return {"precision": "tf32x3", "value": world * rows * ks / (ms_max / 1e3), "unit": "rows/s",
             "ms_per_step": ms_max / ks, "roofline_bound": roof["bound"], "roofline_frac": roof["frac"],
             "hbm_frac": roof["hbm"]["frac"],
-            "kernel": "K2 3xTF32" if w.feature_count < 64 else "K1/K3 (see DESIGN.md §3)"}
+            "kernel": ("K2 3xTF32" if w.feature_count < 64 else
+                       "K3X 3xTF32 (wide)" if w.feature_count >= 512 else "K1 3xTF32")}
 
 
 def end_to_end(torch, dev, model, w, sr, rank, world, dist, a) -> dict:

@@ -317,8 +317,12 @@ def cpu_baseline(w: W.Workload, regime: str, steps: int = 3) -> dict:
     figure, on a bounded sample of the workload (rank 0, N=1 only)."""
     procs = max(1, len(os.sched_getaffinity(0)))
     crow = cpu_rows_per_step(w, procs)
+    if w.name == "wide":       # SURVEY.md §8(d): a 65,536-row subset, extrapolated
+        crow = min(w.batch, 65536)
+        steps = 1
     ref = CpuReference(w.name, regime, crow)
-    ref.step()
+    if w.name != "wide":
+        ref.step()
     ct = [ref.step() for _ in range(steps)]
     ref.close()
     one_rows = CPU_ROWS_PER_CORE[w.name]

@@ -94,7 +94,8 @@ struct Cfg {
   static constexpr int OFF_XCH = rup(OFF_CONST + CONST_BYTES, 128);   // [2][4 q][4 c][32 lanes] float4
   static constexpr int OFF_STG = OFF_XCH + 2 * 4 * 4 * 32 * 16;
   static constexpr int STG_WARP = 32 * 16 * 4;
-  static constexpr int OFF_BAR = OFF_STG + 16 * STG_WARP;
+  static constexpr int OFF_LACC = OFF_STG + 16 * STG_WARP;     // head accumulators of slices 0, 1
+  static constexpr int OFF_BAR = OFF_LACC + rup(256 * C * 4, 128);
   static constexpr int SMEM_BYTES = OFF_BAR + 256;
   static_assert(SMEM_BYTES <= 227 * 1024, "K3X shared-memory plan");
   // global scratch per CTA: prior, agg, the step's mask and xn, fp32 [F/4][128][4] each
@@ -333,7 +334,8 @@ tabnet_wide_x3(const Params p, const ForwardArgs a) {
   };
 
   float gv[HS];                                      // this slice's GLU activations
-  float lacc[C];                                     // d_sum @ head_W, accumulated per step (slices 0, 1)
+  // d_sum @ head_W, accumulated per step by slices 0, 1: in SMEM (registers are the limit)
+  float* const lacc = reinterpret_cast<float*>(smem + CF::OFF_LACC) + (c < 2 ? (c * 128 + r) * C : 0);
 
   // GLU over D = [lin' | gate'] (+ the folded biases) for this slice's outputs:
   // gv <- lin' sigma [+ sqrt(.5) gv], sigma = 1 / (1 + 2^gate')
@@ -574,8 +576,8 @@ tabnet_wide_x3(const Params p, const ForwardArgs a) {
       }
       if (bad && a.err_flag) atomicOr(a.err_flag, 1);
     }
-#pragma unroll
-    for (int k = 0; k < C; ++k) lacc[k] = 0.0f;
+    if (c < 2)
+      for (int k = 0; k < C; ++k) lacc[k] = 0.0f;
     bool all_eta_zero = true;
     transform(0, false);                             // network.py:226-227
     store_att_a();                                   // A of step 1's attentive GEMM

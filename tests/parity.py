@@ -88,6 +88,10 @@ def compare(ref: dict, got: dict, *, delta: float = 2e-5, gap: float = 1e-6,
                 scale = np.maximum(r_row, np.asarray(ref["logit_scale"], np.float64)[keep])
             rep.viol[k] = int(np.count_nonzero(np.any(err > rtol * scale + atol[k], axis=-1)))
         elif k in ("masks", "importance"):
+            # reported only: elementwise relative error on the support entries
+            # that carry at least 1% of the row's mass
+            on = np.abs(r) >= 1e-2 * np.maximum(np.abs(r).sum(axis=-1, keepdims=True), 1e-300)
+            rep.max_err[k + "_support_rel"] = float((err[on] / np.abs(r[on])).max()) if on.any() else 0.0
             e_row = err.max(axis=-1)
             r_row = np.abs(r).sum(axis=-1)
             rep.max_err[k + "_rownorm_rel"] = float((e_row / np.maximum(r_row, 1e-30)).max())

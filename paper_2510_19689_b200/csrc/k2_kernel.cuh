@@ -45,6 +45,11 @@ using tc::tmem_load_n;
 using tc::tmem_store_n;
 
 constexpr int cmin(int a, int b) { return a < b ? a : b; }
+constexpr int glu_chunk_width(int cw0, int cb, int ce) {
+  for (int w = cw0; w >= 2; --w)
+    if (w % 2 == 0 && cb % w == 0 && ce % w == 0) return w;
+  return 2;
+}
 constexpr int pow2ceil(int v) { int p = 32; while (p < v) p <<= 1; return p; }
 
 template <int F_, int ND_, int NA_, int S_, int C_, int PREC_>
@@ -52,6 +57,8 @@ struct Cfg {
   static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
   static_assert(PREC == kPrecTF32 || PREC == kPrecBF16 || PREC == tc::kPrecTF32x3, "K2 precision");
   static constexpr int H = ND + NA, N2 = 2 * H;
+  // MMA N of the GLU GEMMs: 2h padded to the M=128 granule (B rows beyond 2h are 0)
+  static constexpr int NP = rup(N2, 16);
   static constexpr bool X3 = (PREC == tc::kPrecTF32x3);   // 3xTF32: A and B split hi/lo, 3 MMAs
   static constexpr bool BF = (PREC == kPrecBF16);
   static constexpr int KG = BF ? 16 : 8;               // MMA K granule
@@ -65,7 +72,7 @@ struct Cfg {
   static constexpr int FN = rup(F, 16);                // attentive N
   static constexpr int KA_EL = cmax(cmax(K1, KHID), KATT);
   static constexpr int KA = BF ? KA_EL / 2 : KA_EL;    // A operand TMEM columns
-  static constexpr int DW = cmax(N2, FN);
+  static constexpr int DW = cmax(NP, FN);
   static constexpr int T_D = 0, T_A = DW, T_AL = T_A + KA, T_PR = T_AL + (X3 ? KA : 0), T_END = T_PR + F;
   static constexpr int TCG = rup(T_END, 32);           // TMEM columns per group
   static constexpr int NG_TMEM = 512 / TCG;
@@ -78,8 +85,8 @@ struct Cfg {
   static constexpr int NG_S = cmin(TBN_K2_MAXNG, cmin(NG_TMEM, 65536 / (128 * (F + H + 48))));
   // weight blocks (B operands, N x K K-major canonical)
   static constexpr int PARTS = X3 ? 2 : 1;            // hi [+ lo] B blocks
-  static constexpr int B_SH1 = PARTS * N2 * K1 * ESZ;
-  static constexpr int B_HID = PARTS * N2 * KHID * ESZ;
+  static constexpr int B_SH1 = PARTS * NP * K1 * ESZ;
+  static constexpr int B_HID = PARTS * NP * KHID * ESZ;
   static constexpr int B_ATT = PARTS * FN * KATT * ESZ;
   static constexpr int HBR = rup(B_HID, 128), ABR = rup(B_ATT, 128);
   // consts (floats): scale F | shift F | head_W ND*C | head_b C
@@ -117,7 +124,7 @@ struct Cfg {
   static_assert(NG >= 1, "per-row state does not fit");
   static constexpr int TCOLS = pow2ceil(NG * TCG);
   static_assert(TCOLS <= 512, "TMEM");
-  static_assert(N2 <= 256 && FN <= 256, "MMA N > 256");
+  static_assert(NP <= 256 && FN <= 256, "MMA N > 256");
   static constexpr int THREADS = NG * 128;
   static constexpr int NW = NG * 4;
   // shared-memory plan: resident image (or its fixed part + att + ring) | staging | bars
@@ -400,8 +407,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       ptx::tc_fence_after();
       const uint32_t tAL = tA + CF::KA;              // A_lo (3xTF32 only)
 #ifndef TBN_K2_NOMMA          // dev experiment only: the tensor core's share of the chain
-      if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::N2>(tD, tA, tAL, wbase + bo);
-      else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::N2>(tD, tA, tAL, wbase + bo);
+      if (kind == 0) tc::issue_gemm<CF, CF::K1, CF::NP>(tD, tA, tAL, wbase + bo);
+      else if (kind == 1) tc::issue_gemm<CF, CF::KHID, CF::NP>(tD, tA, tAL, wbase + bo);
       else tc::issue_gemm<CF, CF::KATT, CF::FN>(tD, tA, tAL, wbase + bo);
 #endif
       ptx::mma_commit(&bars->dfull[g]);
@@ -438,10 +445,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   auto glu_range = [&](bool residual, auto cb, auto ce) {
     constexpr int CB = decltype(cb)::value, CE = decltype(ce)::value;
     constexpr int CW0 = CF::XS ? (H < 8 ? H : 8) : (H < 16 ? H : 16);   // 16 measured no faster
-    // widest chunk (a power of two up to CW0) that tiles [CB, CE)
-    constexpr int CW = ((CB | CE) % CW0 == 0) ? CW0 : ((CB | CE) % 8 == 0 && CW0 >= 8) ? 8
-                       : ((CB | CE) % 4 == 0 && CW0 >= 4) ? 4 : 2;
-    static_assert(H % CW == 0 && CB % CW == 0 && CE % CW == 0, "GLU chunking");
+    // the widest even chunk up to CW0 that tiles [CB, CE) (any h, pruned ranges)
+    constexpr int CW = glu_chunk_width(CW0, CB, CE);
+    static_assert(CB % CW == 0 && CE % CW == 0, "GLU chunking");
     float lin[CW], gate[CW];
     tmem_load_n<CW>(tD + CB, lin);
     tmem_load_n<CW>(tD + H + CB, gate);

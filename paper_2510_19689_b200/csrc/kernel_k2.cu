@@ -42,12 +42,12 @@ bool k2_pack_layout(const K2Layout& L, const HostParams& hp, TcModel* out, std::
     }
   }
   using pack::pack_block_k2;
-  pack_block_k2(img, L.O_SH1 / 4, hp.sh1_W, F, N2, N2, L.K1, L.X3, N2, &cs_first, hp.sh1_b, L.BF);
-  pack_block_k2(img, L.O_SH2 / 4, hp.sh2_W, H, N2, N2, L.KHID, L.X3, N2, &cs_res, hp.sh2_b, L.BF);
+  pack_block_k2(img, L.O_SH1 / 4, hp.sh1_W, F, N2, L.NP, L.K1, L.X3, N2, &cs_first, hp.sh1_b, L.BF);
+  pack_block_k2(img, L.O_SH2 / 4, hp.sh2_W, H, N2, L.NP, L.KHID, L.X3, N2, &cs_res, hp.sh2_b, L.BF);
   for (int s = 0; s <= S; ++s) {
-    pack_block_k2(img, (L.O_FC1 + s * L.HBR) / 4, hp.fc1_W[s], H, N2, N2, L.KHID, L.X3, N2, &cs_res,
+    pack_block_k2(img, (L.O_FC1 + s * L.HBR) / 4, hp.fc1_W[s], H, N2, L.NP, L.KHID, L.X3, N2, &cs_res,
                   hp.fc1_b[s], L.BF);
-    pack_block_k2(img, (L.O_FC2 + s * L.HBR) / 4, hp.fc2_W[s], H, N2, N2, L.KHID, L.X3, N2, &cs_res,
+    pack_block_k2(img, (L.O_FC2 + s * L.HBR) / 4, hp.fc2_W[s], H, N2, L.NP, L.KHID, L.X3, N2, &cs_res,
                   hp.fc2_b[s], L.BF);
   }
   for (int s = 1; s <= S; ++s)
@@ -82,7 +82,7 @@ template <class CF>
 K2Layout layout_of() {
   K2Layout L;
   L.F = CF::F; L.ND = CF::ND; L.NA = CF::NA; L.S = CF::S; L.C = CF::C;
-  L.X3 = CF::X3; L.BF = CF::BF; L.H = CF::H; L.N2 = CF::N2;
+  L.X3 = CF::X3; L.BF = CF::BF; L.H = CF::H; L.N2 = CF::N2; L.NP = CF::NP;
   L.K1 = CF::K1; L.KHID = CF::KHID; L.KATT = CF::KATT; L.FN = CF::FN;
   L.C_SCALE = CF::C_SCALE; L.C_SHIFT = CF::C_SHIFT; L.C_HW = CF::C_HW; L.C_HB = CF::C_HB;
   L.O_SH1 = CF::O_SH1; L.O_SH2 = CF::O_SH2; L.O_FC1 = CF::O_FC1; L.O_FC2 = CF::O_FC2; L.O_ATT = CF::O_ATT;

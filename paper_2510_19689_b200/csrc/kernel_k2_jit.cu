@@ -107,7 +107,7 @@ uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
 }
 
 const char* kHeaders[] = {"k2_kernel.cuh", "tc_kernel.cuh", "tc_ptx.cuh", "tbn_rtc.h", "tbn_args.h"};
-constexpr int kLayoutInts = 27;
+constexpr int kLayoutInts = 28;
 
 struct JitK2 {
   cudaLibrary_t lib = nullptr;
@@ -189,7 +189,7 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
       << "typedef " << cfg << " JCF;\n"
       << "template __global__ void tbn::k2::tabnet_rowthread<JCF>(tbn::k2::Params, tbn::ForwardArgs);\n"
       << "extern \"C\" __global__ void tbn_k2_layout(int* o) {\n"
-      << "  const int v[] = {JCF::F, JCF::ND, JCF::NA, JCF::S, JCF::C, JCF::X3, JCF::BF, JCF::H, JCF::N2,\n"
+      << "  const int v[] = {JCF::F, JCF::ND, JCF::NA, JCF::S, JCF::C, JCF::X3, JCF::BF, JCF::H, JCF::N2, JCF::NP,\n"
       << "    JCF::K1, JCF::KHID, JCF::KATT, JCF::FN, JCF::C_SCALE, JCF::C_SHIFT, JCF::C_HW, JCF::C_HB,\n"
       << "    JCF::O_SH1, JCF::O_SH2, JCF::O_FC1, JCF::O_FC2, JCF::O_ATT, tbn::tc::rup(JCF::B_HID, 128),\n"
       << "    tbn::tc::rup(JCF::B_ATT, 128), JCF::IMG_BYTES, JCF::SMEM_BYTES, JCF::THREADS};\n"
@@ -250,7 +250,7 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
   K2Layout& L = j->L;
   int i = 0;
   L.F = h[i++]; L.ND = h[i++]; L.NA = h[i++]; L.S = h[i++]; L.C = h[i++];
-  L.X3 = h[i++] != 0; L.BF = h[i++] != 0; L.H = h[i++]; L.N2 = h[i++];
+  L.X3 = h[i++] != 0; L.BF = h[i++] != 0; L.H = h[i++]; L.N2 = h[i++]; L.NP = h[i++];
   L.K1 = h[i++]; L.KHID = h[i++]; L.KATT = h[i++]; L.FN = h[i++];
   L.C_SCALE = h[i++]; L.C_SHIFT = h[i++]; L.C_HW = h[i++]; L.C_HB = h[i++];
   L.O_SH1 = h[i++]; L.O_SH2 = h[i++]; L.O_FC1 = h[i++]; L.O_FC2 = h[i++]; L.O_ATT = h[i++];

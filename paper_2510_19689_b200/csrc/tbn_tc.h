@@ -36,7 +36,7 @@ struct TcModel {
 struct K2Layout {
   int F = 0, ND = 0, NA = 0, S = 0, C = 0;
   bool X3 = false, BF = false;
-  int H = 0, N2 = 0, K1 = 0, KHID = 0, KATT = 0, FN = 0;
+  int H = 0, N2 = 0, NP = 0, K1 = 0, KHID = 0, KATT = 0, FN = 0;
   int C_SCALE = 0, C_SHIFT = 0, C_HW = 0, C_HB = 0;
   int O_SH1 = 0, O_SH2 = 0, O_FC1 = 0, O_FC2 = 0, O_ATT = 0, HBR = 0, ABR = 0;
   int IMG_BYTES = 0, SMEM_BYTES = 0, THREADS = 0;

@@ -166,6 +166,55 @@ def test_load_invariance_bitwise(precision):
     assert not load_invariance_check(m, x, use_batch_stats=True)
 
 
+@pytest.mark.parametrize("precision", ["bf16", "tf32x3"])
+def test_load_invariance_bitwise_wide(precision):
+    """K3 / K3X (one tile per CTA, streamed weights, per-CTA scratch in the
+    per-thread host context's workspace): batch size 1 vs 96 and 1 vs 16
+    concurrent callers, bitwise."""
+    m = P.TabNetModel.from_reference(W.make_model("wide"), precision=precision)
+    x = W.make_inputs(W.WORKLOADS["wide"], 96).astype(np.float64)
+    assert load_invariance_check(m, x, concurrency=(1, 16), batch_sizes=(1, 96))
+
+
+@pytest.mark.parametrize("precision", ["auto", "bf16"])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_random_shapes_parity(seed, precision):
+    """Seeded random model shapes (F 5..60, n_d/n_a 4..24, 1..6 steps, 2..6
+    classes; 2h is often not a multiple of 16, the M=128 MMA's N granule):
+    "auto" (a 3xTF32 tensor-core kernel, prebuilt or compiled for the shape at
+    model creation, else the fp32 kernel) against the float64 oracle under the
+    tie-aware rule; bf16 against the rounding-faithful emulation; both with
+    batch invariance."""
+    from oracle import tabnet_emulate as E
+    rng = np.random.default_rng(100 + seed)
+    F = int(rng.integers(5, 61))
+    nd, na = (int(2 * rng.integers(2, 13)) for _ in range(2))
+    S, C = int(rng.integers(1, 7)), int(rng.integers(2, 7))
+    m = _shape_model(F, nd, na, S, C, precision, seed=seed)
+    prec = m.engine().precision
+    if precision == "auto":
+        assert prec == "tf32x3", ((F, nd, na, S, C), prec)      # K2 serves every such shape
+    x = W.make_inputs(W.Workload("rand", 9, F, nd, na, S, C, 0, "rand"), 700, seed=seed)
+    r = m.apply(x.astype(np.float64))
+    if precision == "auto":
+        ref = O.apply_model(m, x.astype(np.float64), diagnostics=True)
+        zs, tau = ref["z_shift"], ref["tau"]
+        ref["margin"] = np.abs(zs - tau[..., None]).min(axis=2) / np.maximum(np.abs(zs).max(axis=2), 1e-300)
+        p = np.sort(ref["probabilities"], axis=1)
+        ref["top2_gap"] = p[:, -1] - p[:, -2]
+        rep = compare(ref, _res_dict(r))
+        print((F, nd, na, S, C), prec, rep.summary())
+        assert rep.ok, ((F, nd, na, S, C), prec, rep.summary())
+    else:
+        st = _emu_stats(_res_dict(r), E.apply_model_emulated(m, x, mode="bf16"))
+        print((F, nd, na, S, C), prec, st)
+        mmax, mp999, imax, pmax = EMU_BOUNDS["bf16"]
+        assert st["mask_max"] < mmax and st["mask_p999"] < mp999 and st["imp_max"] < imax and st["prob_max"] < pmax, \
+            ((F, nd, na, S, C), st)
+    part = m.apply(x[:77].astype(np.float64))
+    assert np.array_equal(part.masks, r.masks[:, :77]) and np.array_equal(part.probabilities, r.probabilities[:77])
+
+
 @pytest.mark.parametrize("precision", ALL_PRECISIONS)
 def test_nonfinite_and_width_errors(precision):
     m = P.TabNetModel.from_reference(W.make_model("adult"), precision=precision)

@@ -179,6 +179,20 @@ def test_load_invariance_bitwise_wide(precision):
 @pytest.mark.parametrize("precision", ["auto", "bf16"])
 @pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
 def test_random_shapes_parity(seed, precision):
+    _random_shape_case(seed, precision, wide=False)
+
+
+@pytest.mark.parametrize("precision", ["auto", "bf16"])
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_random_shapes_parity_wider(seed, precision):
+    """A wider draw (F up to 120, odd n_d / n_a, up to 8 steps and 12
+    classes): whatever kernel serves the shape ("auto" may land on the fp32
+    CUDA-core kernel where no tensor-core instance fits) must meet the same
+    bar; bf16 is skipped where no bf16 kernel exists (odd widths)."""
+    _random_shape_case(seed, precision, wide=True)
+
+
+def _random_shape_case(seed, precision, wide):
     """Seeded random model shapes (F 5..60, n_d/n_a 4..24, 1..6 steps, 2..6
     classes; 2h is often not a multiple of 16, the M=128 MMA's N granule):
     "auto" (a 3xTF32 tensor-core kernel, prebuilt or compiled for the shape at
@@ -187,12 +201,21 @@ def test_random_shapes_parity(seed, precision):
     batch invariance."""
     from oracle import tabnet_emulate as E
     rng = np.random.default_rng(100 + seed)
-    F = int(rng.integers(5, 61))
-    nd, na = (int(2 * rng.integers(2, 13)) for _ in range(2))
-    S, C = int(rng.integers(1, 7)), int(rng.integers(2, 7))
+    if wide:
+        F = int(rng.integers(5, 121))
+        nd, na = (int(rng.integers(3, 33)) for _ in range(2))
+        S, C = int(rng.integers(1, 9)), int(rng.integers(2, 13))
+    else:
+        F = int(rng.integers(5, 61))
+        nd, na = (int(2 * rng.integers(2, 13)) for _ in range(2))
+        S, C = int(rng.integers(1, 7)), int(rng.integers(2, 7))
     m = _shape_model(F, nd, na, S, C, precision, seed=seed)
-    prec = m.engine().precision
-    if precision == "auto":
+    try:
+        prec = m.engine().precision
+    except P.UnsupportedShapeError:
+        assert precision == "bf16" and wide, (F, nd, na, S, C)
+        pytest.skip(f"no bf16 kernel for {(F, nd, na, S, C)}")
+    if precision == "auto" and not wide:
         assert prec == "tf32x3", ((F, nd, na, S, C), prec)      # K2 serves every such shape
     x = W.make_inputs(W.Workload("rand", 9, F, nd, na, S, C, 0, "rand"), 700, seed=seed)
     r = m.apply(x.astype(np.float64))
@@ -209,6 +232,11 @@ def test_random_shapes_parity(seed, precision):
         st = _emu_stats(_res_dict(r), E.apply_model_emulated(m, x, mode="bf16"))
         print((F, nd, na, S, C), prec, st)
         mmax, mp999, imax, pmax = EMU_BOUNDS["bf16"]
+        if wide:
+            # deeper / wider random models: the tanh.approx and summation-order
+            # gap to the emulation grows with the steps (measured 0.0105 p99.9 at
+            # S = 7, n_a = 26): twice the BASELINE-shape bounds
+            mmax, mp999, imax, pmax = 2 * mmax, 2 * mp999, 2 * imax, 2 * pmax
         assert st["mask_max"] < mmax and st["mask_p999"] < mp999 and st["imp_max"] < imax and st["prob_max"] < pmax, \
             ((F, nd, na, S, C), st)
     part = m.apply(x[:77].astype(np.float64))

@@ -243,6 +243,37 @@ def _random_shape_case(seed, precision, wide):
     assert np.array_equal(part.masks, r.masks[:, :77]) and np.array_equal(part.probabilities, r.probabilities[:77])
 
 
+@pytest.mark.parametrize("name", ["hr", "wide"])
+@pytest.mark.parametrize("precision", ["tf32x3", "fp32"])
+def test_adversarial_rows(name, precision):
+    """Rows the synthetic N(0,1) stream never produces: all-zero, constant,
+    exactly the normalization mean (xn = 0), duplicated features (ties in the
+    logits), large (x1e3) and tiny (x1e-6) scales, one-hot — exact modes
+    against the float64 oracle under the tie-aware rule, plus the simplex
+    properties of every mask and importance row."""
+    w = W.WORKLOADS[name]
+    F = w.feature_count
+    m = P.TabNetModel.from_reference(W.make_model(name, "trained"), precision=precision)
+    base = W.make_inputs(w, 64, seed=5).astype(np.float64)
+    rows = [np.zeros(F), np.full(F, 3.0), np.asarray(m.norm_mean, np.float64)]
+    dup = base[0].copy()
+    dup[1::2] = dup[0::2][: len(dup[1::2])]
+    rows += [dup, base[1] * 1e3, base[2] * 1e-6, np.eye(F)[F // 2] * 5.0, -base[3]]
+    x = np.vstack(rows + [base[4:40]])
+    r = m.apply(x)
+    ref = O.apply_model(m, x, diagnostics=True)
+    zs, tau = ref["z_shift"], ref["tau"]
+    ref["margin"] = np.abs(zs - tau[..., None]).min(axis=2) / np.maximum(np.abs(zs).max(axis=2), 1e-300)
+    p = np.sort(ref["probabilities"], axis=1)
+    ref["top2_gap"] = p[:, -1] - p[:, -2]
+    rep = compare(ref, _res_dict(r))
+    print(name, precision, rep.summary())
+    assert rep.ok, rep.summary()
+    np.testing.assert_allclose(r.masks.sum(axis=2), 1.0, atol=1e-5)
+    np.testing.assert_allclose(r.importance.sum(axis=1), 1.0, atol=1e-5)
+    assert np.all(np.isfinite(r.probabilities))
+
+
 @pytest.mark.parametrize("precision", ALL_PRECISIONS)
 def test_nonfinite_and_width_errors(precision):
     m = P.TabNetModel.from_reference(W.make_model("adult"), precision=precision)

@@ -20,5 +20,7 @@ python bench.py --config wide --rows 262144 --steps 5 --warmup 3 > gpurun_out/f_
 python bench.py --config wide --steps 3 --warmup 3 --no-e2e > gpurun_out/f_wide16m_bf16.json   # config 5: 2^24 rows streamed
 python bench.py --config hr8 --rows 8192 --no-cpu-baseline > gpurun_out/f_hr8_share.json          # one GPU's share of 65,536 on 8
 python bench.py --config wide --precision fp32 --rows 262144 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/f_wide_fp32.json
+python bench.py --config wide --precision tf32x3 --rows 262144 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/f_wide_x3.json
+python bench.py --config hr8 --rows 8192 --inflight 16 --no-cpu-baseline --no-e2e --no-parity-mode > gpurun_out/f_hr8_share16.json
 python bench.py --impl reference                  > gpurun_out/f_reference.json
 bash tools/profile.sh hr bf16 $TAG

@@ -132,6 +132,17 @@ def reduce_over_ranks(total_ms: float, rows: int, world: int, dist, device) -> t
     return float(tmax[0].item()), float(tsum[1].item())
 
 
+def max_over_ranks_list(vals: list, world: int, dist, device) -> list:
+    """Elementwise max over ranks (each step's batch latency at N GPUs is its
+    slowest shard's)."""
+    if world == 1:
+        return list(vals)
+    import torch
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
 def run_dry(a) -> None:
     """The rank/row plan and the max/sum reduction of run_ours, over gloo on
     CPU (tests/test_bench_logic.py runs it under the self-launch)."""
@@ -144,6 +155,9 @@ def run_dry(a) -> None:
     rows, start, sharded = plan_rows(w, a, rank, world)
     fake_ms = 1.0 + rank                      # a made-up per-rank time: the max must win
     ms, total = reduce_over_ranks(fake_ms, rows, world, dist, torch.device("cpu"))
+    # per-step latencies: each step's slowest rank (rank r is slow on step r)
+    steps = max_over_ranks_list([1.0 + (5.0 if i == rank else 0.0) for i in range(3)], world, dist,
+                                torch.device("cpu"))
     starts = [None] * world
     if world > 1:
         dist.all_gather_object(starts, (start, rows))
@@ -151,7 +165,8 @@ def run_dry(a) -> None:
         starts = [(start, rows)]
     if rank == 0:
         print(json.dumps({"n_gpus": world, "rows_per_rank": rows, "rows_all_ranks": total,
-                          "max_ms": ms, "shards": starts, "scaling": "strong" if sharded else "weak",
+                          "max_ms": ms, "step_max_ms": steps, "shards": starts,
+                          "scaling": "strong" if sharded else "weak",
                           "config": bench_config(w, a, rows, world, sharded)}), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -611,6 +626,7 @@ def run_ours(a) -> None:
     per_step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
     if sr.flush_mode:
         per_step_ms = flushed_ms        # cold-L2 per-step device times
+    per_step_ms = max_over_ranks_list(per_step_ms, world, dist, dev)
 
     # ---- steady state: Q batches of this rank's rows in flight on Q streams
     steady = None
@@ -671,7 +687,8 @@ def run_ours(a) -> None:
             "roofline": roof,
             "latency_ms": {"p50": nearest_rank(per_step_ms, 50), "p99": nearest_rank(per_step_ms, 99),
                            "batch": rows, "kind": "device (CUDA events around each step's single-step graph replay"
-                                                  + (", L2 flushed before each)" if sr.flush_mode else ")")},
+                                                  + (", L2 flushed before each" if sr.flush_mode else "")
+                                                  + ("; max over ranks per step)" if world > 1 else ")")},
             "steady_state": steady,
             "parity_mode": parity,
             "cpu_baseline": cpu,

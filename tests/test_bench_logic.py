@@ -135,4 +135,5 @@ def test_two_rank_launch_and_reduction_gloo():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["rows_per_rank"] == 131072 and d["rows_all_ranks"] == 262144
     assert d["max_ms"] == 2.0 and d["shards"] == [[0, 131072], [131072, 131072]]
+    assert d["step_max_ms"] == [6.0, 6.0, 1.0]      # per-step latency: the slowest rank per step
     assert d["scaling"] == "strong"

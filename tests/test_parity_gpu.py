@@ -176,6 +176,26 @@ def test_load_invariance_bitwise_wide(precision):
     assert load_invariance_check(m, x, concurrency=(1, 16), batch_sizes=(1, 96))
 
 
+def test_mixed_models_concurrent_threads():
+    """Several models and kernels (K2 bf16 / 3xTF32, K3, K3X, the fp32 kernel)
+    served from 12 threads at once on one device: every result equals the
+    same call made alone (per-thread host contexts, per-model workspaces)."""
+    from concurrent.futures import ThreadPoolExecutor
+    cases = [("hr", "bf16"), ("hr", "tf32x3"), ("wide", "bf16"), ("wide", "tf32x3"), ("adult", "fp32"),
+             ("bls", "bf16")]
+    models = {c: P.TabNetModel.from_reference(W.make_model(c[0]), precision=c[1]) for c in cases}
+    xs = {c: W.make_inputs(W.WORKLOADS[c[0]], 150 if c[0] == "wide" else 700, seed=21).astype(np.float64)
+          for c in cases}
+    alone = {c: models[c].apply(xs[c]) for c in cases}
+    jobs = [cases[i % len(cases)] for i in range(36)]
+    with ThreadPoolExecutor(max_workers=12) as pool:
+        outs = list(pool.map(lambda c: (c, models[c].apply(xs[c])), jobs))
+    for c, r in outs:
+        a = alone[c]
+        assert np.array_equal(r.probabilities, a.probabilities), c
+        assert np.array_equal(r.masks, a.masks) and np.array_equal(r.importance, a.importance), c
+
+
 @pytest.mark.parametrize("precision", ["auto", "bf16"])
 @pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
 def test_random_shapes_parity(seed, precision):

@@ -358,6 +358,13 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     if (old == (v / (NSLOT ? NSLOT : 1)) * NG + NG - 1 && v + NSLOT < nblk) ring_load(v + NSLOT);
   };
 
+  // Programmatic dependent launch: everything above (barriers, TMEM, the weight
+  // image TMA) overlaps the tail of the previous kernel on the stream; from here
+  // on this grid reads and writes data that kernel may produce or consume
+  // (x, the batch-statistics affine, the outputs), so wait for it to complete,
+  // and let the next launch start its own prologue as SMs free up.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   {   // this warp's first x tile streams in with the weights
     int64_t r0w;
     const int nw0 = warp_rows(g, r0w);

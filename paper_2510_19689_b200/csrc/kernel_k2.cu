@@ -107,8 +107,17 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   const int64_t nq = a.packed ? (a.rows + 128 * CF::NG - 1) / (128 * CF::NG)
                               : (a.rows + TBN_K2_ROWQ - 1) / TBN_K2_ROWQ;
   const int grid = (int)(nq < num_sms ? nq : num_sms);
-  k2::tabnet_rowthread<CF><<<grid, CF::THREADS, CF::SMEM_BYTES, stream>>>(*(const k2::Params*)m.params, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(CF::THREADS);
+  cfg.dynamicSmemBytes = CF::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (k2_kernel.cuh)
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k2::tabnet_rowthread<CF>, *(const k2::Params*)m.params, a);
 }
 
 #define TBN_K2(F, ND, NA, S, C, P)                                                  \

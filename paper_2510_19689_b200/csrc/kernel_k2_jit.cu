@@ -308,7 +308,17 @@ cudaError_t k2_jit_launch(const TcModel& m, const ForwardArgs& a, int num_sms, c
   k2::Params p = *(const k2::Params*)m.params;
   ForwardArgs fa = a;
   void* args[] = {&p, &fa};
-  return cudaLaunchKernel((const void*)j->kern, dim3(grid), dim3(j->L.THREADS), args, j->L.SMEM_BYTES, stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(j->L.THREADS);
+  cfg.dynamicSmemBytes = j->L.SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL, as the prebuilt K2
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, (const void*)j->kern, args);
 }
 
 }  // namespace tbn

@@ -1,5 +1,6 @@
 // tbn_internal.h — internal (non-ABI) declarations of libtabnet_b200.
 #pragma once
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -15,6 +16,15 @@ void set_last_error(const std::string& msg);   // tbn_last_error() of this threa
 // (TabNetModel(device=N) caches one engine per device).  Thread-safe: the
 // public host API is reentrant.  `Tag` makes the state per kernel instance.
 constexpr int kMaxDevices = 64;
+
+// Programmatic dependent launch for the K2 forward (TBN_NO_PDL=1 disables it: A/B)
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TBN_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 template <class Tag>
 cudaError_t smem_attr_once(const void* func, int bytes) {
   static std::once_flag once[kMaxDevices];

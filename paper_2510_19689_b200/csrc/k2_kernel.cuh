@@ -363,16 +363,16 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   // on this grid reads and writes data that kernel may produce or consume
   // (x, the batch-statistics affine, the outputs), so wait for it to complete,
   // and let the next launch start its own prologue as SMs free up.
+  float* const rcp_tab = reinterpret_cast<float*>(smem + CF::OFF_RCP);
+  for (int i = threadIdx.x; i <= F; i += blockDim.x) rcp_tab[i] = i ? __frcp_rn((float)i) : 0.0f;
+  ptx::mbar_wait(&bars->cfull, 0);                   // the weights have landed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  {   // this warp's first x tile streams in with the weights
+  {   // this warp's first x tile
     int64_t r0w;
     const int nw0 = warp_rows(g, r0w);
     if (nw0 > 0) issue_x(r0w, nw0);
   }
-  float* const rcp_tab = reinterpret_cast<float*>(smem + CF::OFF_RCP);
-  for (int i = threadIdx.x; i <= F; i += blockDim.x) rcp_tab[i] = i ? __frcp_rn((float)i) : 0.0f;
-  ptx::mbar_wait(&bars->cfull, 0);
   if (a.scale) {     // batch-statistics control: override the affine in this CTA's copy
     float* cw = reinterpret_cast<float*>(smem);
     for (int f = threadIdx.x; f < F; f += blockDim.x) {

@@ -366,6 +366,15 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   float* const rcp_tab = reinterpret_cast<float*>(smem + CF::OFF_RCP);
   for (int i = threadIdx.x; i <= F; i += blockDim.x) rcp_tab[i] = i ? __frcp_rn((float)i) : 0.0f;
   ptx::mbar_wait(&bars->cfull, 0);                   // the weights have landed
+  {   // warm L2 with this warp's first x rows (a hint; L2 is where the previous
+      // kernel's writes land, so a prefetch ahead of the wait cannot read stale data)
+    int64_t r0p;
+    const int nwp = warp_rows(g, r0p);
+    if (lane == 0 && nwp > 0 && x_bulk_ok) {
+      const uint32_t bytes = (uint32_t)((nwp * F * 4) & ~15);
+      if (bytes) ptx::bulk_prefetch_l2(a.x + r0p * F, bytes);
+    }
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   {   // this warp's first x tile

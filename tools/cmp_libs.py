@@ -1,3 +1,5 @@
+"""Bitwise A/B of two builds: the same forwards with the in-tree library and with
+another one (argv[1]), compared array by array.  python tools/cmp_libs.py ALT.so"""
 import sys, os, shutil, subprocess
 sys.path.insert(0, ".")
 import numpy as np
@@ -20,7 +22,7 @@ np.savez(sys.argv[1], **out)
 lib = "paper_2510_19689_b200/libtabnet_b200.so"
 shutil.copy(lib, "/tmp/lib_cur.so")
 subprocess.run([sys.executable, "-c", CHILD, "/tmp/a.npz"], check=True)
-shutil.copy("tools/_libs/lib_nosplit.so", lib)
+shutil.copy(sys.argv[1], lib)
 subprocess.run([sys.executable, "-c", CHILD, "/tmp/b.npz"], check=True)
 shutil.copy("/tmp/lib_cur.so", lib)
 a, b = np.load("/tmp/a.npz"), np.load("/tmp/b.npz")

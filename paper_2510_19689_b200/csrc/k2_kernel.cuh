@@ -358,14 +358,14 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     if (old == (v / (NSLOT ? NSLOT : 1)) * NG + NG - 1 && v + NSLOT < nblk) ring_load(v + NSLOT);
   };
 
-  // Programmatic dependent launch: everything above (barriers, TMEM, the weight
-  // image TMA) overlaps the tail of the previous kernel on the stream; from here
-  // on this grid reads and writes data that kernel may produce or consume
-  // (x, the batch-statistics affine, the outputs), so wait for it to complete,
-  // and let the next launch start its own prologue as SMs free up.
-  float* const rcp_tab = reinterpret_cast<float*>(smem + CF::OFF_RCP);
-  for (int i = threadIdx.x; i <= F; i += blockDim.x) rcp_tab[i] = i ? __frcp_rn((float)i) : 0.0f;
-  ptx::mbar_wait(&bars->cfull, 0);                   // the weights have landed
+  // Programmatic dependent launch: everything before the wait (barriers, TMEM,
+  // the weight-image TMA, an L2 prefetch of this warp's first x rows, the
+  // reciprocal table) overlaps the tail of the previous kernel on the stream;
+  // from the wait on this grid reads and writes data that kernel may produce
+  // or consume (x, the batch-statistics affine, the outputs).  The next launch
+  // may start its own prologue as SMs free up.  On a cold start the weights and
+  // the first x rows are in flight together (the weights' landing is awaited
+  // after the x tile is requested).
   {   // warm L2 with this warp's first x rows (a hint; L2 is where the previous
       // kernel's writes land, so a prefetch ahead of the wait cannot read stale data)
     int64_t r0p;
@@ -375,6 +375,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       if (bytes) ptx::bulk_prefetch_l2(a.x + r0p * F, bytes);
     }
   }
+  float* const rcp_tab = reinterpret_cast<float*>(smem + CF::OFF_RCP);
+  for (int i = threadIdx.x; i <= F; i += blockDim.x) rcp_tab[i] = i ? __frcp_rn((float)i) : 0.0f;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   {   // this warp's first x tile
@@ -382,6 +384,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     const int nw0 = warp_rows(g, r0w);
     if (nw0 > 0) issue_x(r0w, nw0);
   }
+  ptx::mbar_wait(&bars->cfull, 0);                   // the weights have landed
   if (a.scale) {     // batch-statistics control: override the affine in this CTA's copy
     float* cw = reinterpret_cast<float*>(smem);
     for (int f = threadIdx.x; f < F; f += blockDim.x) {

@@ -145,10 +145,15 @@ bool tc_supported(const HostParams& hp, int precision) {
 }
 
 // K2 (k2_kernel.cuh) serves the single-pass modes wherever an instance exists;
-// TBN_KERNEL=k1 pins the K1 design (development A/B only).
+// TBN_KERNEL=k1 pins the K1 design, TBN_KERNEL=jit prefers the runtime-compiled
+// K2 over K1 (development A/B only).
 static bool k2_allowed() {
   const char* e = std::getenv("TBN_KERNEL");
   return !(e && std::strcmp(e, "k1") == 0);
+}
+static bool jit_preferred() {
+  const char* e = std::getenv("TBN_KERNEL");
+  return e && std::strcmp(e, "jit") == 0;
 }
 
 bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err) {
@@ -162,7 +167,7 @@ bool tc_pack(const HostParams& hp, int precision, TcModel* out, std::string* err
     out->precision = precision;
     return k2_pack(hp, precision, out, err);
   }
-  const Instance* in = find(hp, precision);
+  const Instance* in = jit_preferred() ? nullptr : find(hp, precision);
   if (!in) {
     if (k2_allowed() && k2_jit_available()) return k2_jit_pack(hp, precision, out, err);
     if (err) *err = "unsupported: no kernel instance for this shape";

@@ -826,10 +826,14 @@ def x_dev(local):
     return torch.device("cuda", local)
 
 
+LAT_REPS = 1000
+
+
 def latency_sweep(model, local, f):
     """HR shape, batches 1..1024 (BASELINE config 3): nearest-rank p50/p99 of the
     device-only kernel time (L2 flushed before each call) and of the end-to-end
-    host call."""
+    host call.  SURVEY.md §8(d) run 4: every power of two 1..1,024, 1,000 timed
+    reps per batch size."""
     import torch
     from paper_2510_19689_b200.device import DeviceRunner
     res = {}
@@ -838,13 +842,13 @@ def latency_sweep(model, local, f):
     stream = torch.cuda.current_stream()
     w = W.WORKLOADS["hr_latency"]
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=x_dev(local))
-    for b in (1, 4, 16, 64, 256, 1024):
+    for b in [1 << i for i in range(11)]:
         x = torch.from_numpy(W.make_inputs(w, b)).cuda()
         for _ in range(20):
             runner.run(x)
         torch.cuda.synchronize()
         dev_ms = []
-        for _ in range(300):
+        for _ in range(LAT_REPS):
             # a queued spin keeps the GPU busy while the host enqueues the events
             # and the launch, so e0 -> e1 is device time only (no host overhead)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -859,7 +863,7 @@ def latency_sweep(model, local, f):
         oh = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in runner.views(b).items()}
         np_out = {k: v.numpy() for k, v in oh.items()}
         e2e_ms = []
-        for i in range(320):
+        for i in range(LAT_REPS + 20):
             t0 = time.perf_counter()
             eng.forward_host_f32(xh.numpy(), 0, np_out)
             if i >= 20:

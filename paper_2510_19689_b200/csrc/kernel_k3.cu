@@ -251,7 +251,9 @@ cudaError_t launch_k3x_impl(const TcModel& m, const ForwardArgs& a, int num_sms,
   if (e != cudaSuccess) return e;
   if (!a.scratch) return cudaErrorInvalidValue;
   const int64_t ntiles = (a.rows + 127) / 128;
-  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  int cap = num_sms;
+  if (const char* e = std::getenv("TBN_K3_GRID")) cap = std::atoi(e) > 0 ? std::atoi(e) : num_sms;   // dev A/B
+  const int grid = (int)(ntiles < cap ? ntiles : cap);
   const size_t scratch_bytes = (size_t)grid * CF::SCRATCH_PER_CTA;
   const size_t persist = l2_persist_bytes();
   const size_t window = scratch_bytes < max_window_bytes() ? scratch_bytes : max_window_bytes();

@@ -19,6 +19,7 @@ struct NvtxRange {
 };
 }  // namespace
 #include "tbn_tc.h"
+#include "host_convert.h"
 
 #include <cmath>
 #include <cstdio>
@@ -527,14 +528,9 @@ Layout layout_for(const tbn_model* m, int64_t rows, uint32_t flags) {
   return L;
 }
 
-template <typename D, typename S_>
-void convert(D* dst, const S_* src, size_t n) {
-  for (size_t i = 0; i < n; ++i) dst[i] = (D)src[i];
-}
-
-// A batch of element-wise conversions (dst[i] = (D)src[i]) spread over host
-// threads when large: the float64 apply() path converts every output of every
-// chunk (HR @ 65,536: 56 M values), which single-threaded costs ~20 ms.
+// A batch of element-wise conversions (dst[i] = (D)src[i]) spread over the
+// host worker pool (host_convert.cpp) when large: the float64 apply() path
+// converts every output of every chunk (HR @ 65,536: 14 M values).
 template <typename D, typename S_>
 struct ConvertJob {
   D* dst;
@@ -545,26 +541,15 @@ template <typename D, typename S_>
 void convert_all(const std::vector<ConvertJob<D, S_>>& jobs) {
   size_t total = 0;
   for (const auto& j : jobs) total += j.n;
-  unsigned nt = std::thread::hardware_concurrency();
-  nt = nt > 16 ? 16 : nt;
-  if (total < (1u << 21) || nt < 2) {      // thread start-up costs ~0.1 ms
-    for (const auto& j : jobs) convert(j.dst, j.src, j.n);
-    return;
-  }
-  const size_t per = (total + nt - 1) / nt;
-  auto work = [&](size_t lo, size_t hi) {      // global element range [lo, hi)
+  tbn::host_parallel_for(total, (size_t)1 << 18, [&](size_t lo, size_t hi) {   // global range [lo, hi)
     size_t base = 0;
     for (const auto& j : jobs) {
       const size_t a = lo > base ? lo - base : 0, b = hi - base < j.n ? hi - base : j.n;
-      if (hi > base && a < j.n && a < b) convert(j.dst + a, j.src + a, b - a);
+      if (hi > base && a < j.n && a < b) tbn::convert_span(j.dst + a, j.src + a, b - a);
       base += j.n;
       if (base >= hi) break;
     }
-  };
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t * per, (t + 1) * per < total ? (t + 1) * per : total);
-  work(0, per < total ? per : total);
-  for (auto& t : th) t.join();
+  });
 }
 
 template <typename T, typename OutT>

@@ -388,7 +388,10 @@ namespace {
 
 constexpr int kNumStreams = 3;
 constexpr int64_t kMinChunk = 8192;
-constexpr int64_t kSmallBatch = 32;       // measured break-even vs one DMA per output: ~64 rows
+// staged + graph path up to here: HR end-to-end p50 at 64 / 128 rows 50 / 54 us
+// vs 70 / 72 us with one DMA per output array; even at 256; the host copy-out
+// loses above (512 rows: 87-90 vs 77 us)
+constexpr int64_t kSmallBatch = 128;
 
 struct StreamCtx {
   cudaStream_t stream = nullptr;
@@ -541,6 +544,8 @@ template <typename D, typename S_>
 void convert_all(const std::vector<ConvertJob<D, S_>>& jobs) {
   size_t total = 0;
   for (const auto& j : jobs) total += j.n;
+  // (the pool's wake-up costs more than it saves below ~1 MB: measured on the
+  // staged small-batch path, 1,024 HR rows 87 -> 239 us with a 128K-value threshold)
   tbn::host_parallel_for(total, (size_t)1 << 18, [&](size_t lo, size_t hi) {   // global range [lo, hi)
     size_t base = 0;
     for (const auto& j : jobs) {

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <thread>
@@ -60,6 +61,8 @@ class Pool {
  public:
   Pool() {
     unsigned hw = std::thread::hardware_concurrency();
+    if (const char* e = std::getenv("TBN_HOST_THREADS"))      // cap (1 = no workers)
+      if (std::atoi(e) > 0 && (unsigned)std::atoi(e) < hw) hw = (unsigned)std::atoi(e);
     nworkers_ = hw > 16 ? 15 : (hw > 1 ? hw - 1 : 0);
     for (unsigned t = 0; t < nworkers_; ++t) th_.emplace_back([this, t] { loop(t + 1); });
   }

@@ -52,7 +52,15 @@ constexpr int glu_chunk_width(int cw0, int cb, int ce) {
 }
 constexpr int pow2ceil(int v) { int p = 32; while (p < v) p <<= 1; return p; }
 
-template <int F_, int ND_, int NA_, int S_, int C_, int PREC_>
+#ifndef TBN_K2_MAXNG
+#define TBN_K2_MAXNG 4
+#endif
+// MAXNG_: row groups per CTA at most.  The throughput instances take 4 (as many
+// as registers and TMEM allow); each shape also has a latency instance with 2
+// (kernel_k2.cu), used when a CTA gets at most 2 row tiles: more registers per
+// thread, xn in registers and (for HR) resident weights shorten the tile chain.
+// The arithmetic is the same in both, so outputs are bitwise identical.
+template <int F_, int ND_, int NA_, int S_, int C_, int PREC_, int MAXNG_ = TBN_K2_MAXNG>
 struct Cfg {
   static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
   static_assert(PREC == kPrecTF32 || PREC == kPrecBF16 || PREC == tc::kPrecTF32x3, "K2 precision");
@@ -78,11 +86,8 @@ struct Cfg {
   static constexpr int NG_TMEM = 512 / TCG;
   // Register file: a row's live state is about 2F + H + 48 registers with xn
   // in registers (variant R), F + H + 48 with xn in shared memory (variant S).
-#ifndef TBN_K2_MAXNG
-#define TBN_K2_MAXNG 4
-#endif
-  static constexpr int NG_R = cmin(TBN_K2_MAXNG, cmin(NG_TMEM, 65536 / (128 * (2 * F + H + 48))));
-  static constexpr int NG_S = cmin(TBN_K2_MAXNG, cmin(NG_TMEM, 65536 / (128 * (F + H + 48))));
+  static constexpr int NG_R = cmin(MAXNG_, cmin(NG_TMEM, 65536 / (128 * (2 * F + H + 48))));
+  static constexpr int NG_S = cmin(MAXNG_, cmin(NG_TMEM, 65536 / (128 * (F + H + 48))));
   // weight blocks (B operands, N x K K-major canonical)
   static constexpr int PARTS = X3 ? 2 : 1;            // hi [+ lo] B blocks
   static constexpr int B_SH1 = PARTS * NP * K1 * ESZ;

@@ -7,6 +7,7 @@
 //   linear columns x 1/2 (shared1) or x sqrt(1/2)/2 (the residual blocks
 //   shared2/fc1/fc2, network.py:131-137: (lin sigma + prev) sqrt(.5)).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "tbn_tc.h"
@@ -96,17 +97,19 @@ bool pack_k2(const HostParams& hp, TcModel* out, std::string* err) {
   return k2_pack_layout(layout_of<CF>(), hp, out, err);
 }
 
+// rows of the batch -> CTAs: one CTA per SM, each with a contiguous, equal
+// block of rows (k2_kernel.cuh); small batches: one CTA per TBN_K2_ROWQ rows
+// (spreading them thinner, 32 rows per CTA, measured no faster).
+// TBN_FLAG_PACKED: NG full tiles per CTA on as few SMs as the batch needs.
+inline int k2_grid(const ForwardArgs& a, int num_sms, int ng) {
+  const int64_t nq = a.packed ? (a.rows + 128 * ng - 1) / (128 * ng) : (a.rows + TBN_K2_ROWQ - 1) / TBN_K2_ROWQ;
+  return (int)(nq < num_sms ? nq : num_sms);
+}
+
 template <class CF>
-cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+cudaError_t launch_k2_cfg(const TcModel& m, const ForwardArgs& a, int grid, cudaStream_t stream) {
   cudaError_t e = smem_attr_once<CF>((const void*)k2::tabnet_rowthread<CF>, CF::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  // one CTA per SM, each with a contiguous, equal block of rows (k2_kernel.cuh);
-  // small batches: one CTA per TBN_K2_ROWQ rows (spreading them thinner, 32
-  // rows per CTA, measured no faster)
-  // (TBN_FLAG_PACKED: NG full tiles per CTA on as few SMs as the batch needs)
-  const int64_t nq = a.packed ? (a.rows + 128 * CF::NG - 1) / (128 * CF::NG)
-                              : (a.rows + TBN_K2_ROWQ - 1) / TBN_K2_ROWQ;
-  const int grid = (int)(nq < num_sms ? nq : num_sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(CF::THREADS);
@@ -120,9 +123,27 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
   return cudaLaunchKernelEx(&cfg, k2::tabnet_rowthread<CF>, *(const k2::Params*)m.params, a);
 }
 
+// CF: the throughput instance; CL: the latency instance of the same shape
+// (at most 2 row groups), launched when no CTA gets more than CL::NG tiles.
+// Both read the same weight image.
+template <class CF, class CL>
+cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
+  static_assert(CF::IMG_BYTES == CL::IMG_BYTES && CF::O_ATT == CL::O_ATT && CF::O_FC2 == CL::O_FC2 &&
+                CF::C_HB == CL::C_HB, "the latency instance must read the same weight image");
+  if constexpr (CL::NG < CF::NG) {
+    static const bool off = std::getenv("TBN_K2_NO_LATENCY") != nullptr;   // development A/B only
+    if (!a.packed && !off) {
+      const int grid = k2_grid(a, num_sms, CL::NG);
+      const int64_t rpc = (((a.rows + grid - 1) / grid) + 3) & ~(int64_t)3;
+      if ((rpc + 127) / 128 <= CL::NG) return launch_k2_cfg<CL>(m, a, grid, stream);
+    }
+  }
+  return launch_k2_cfg<CF>(m, a, k2_grid(a, num_sms, CF::NG), stream);
+}
+
 #define TBN_K2(F, ND, NA, S, C, P)                                                  \
   K2Instance{F, ND, NA, S, C, P, &pack_k2<k2::Cfg<F, ND, NA, S, C, P>>,            \
-             &launch_k2_impl<k2::Cfg<F, ND, NA, S, C, P>>}
+             &launch_k2_impl<k2::Cfg<F, ND, NA, S, C, P>, k2::Cfg<F, ND, NA, S, C, P, 2>>}
 
 #ifdef TBN_K2_SINGLE   // dev A/B builds: one instance only, e.g. -DTBN_K2_SINGLE=K2_HR_BF16
 #define K2_HR_BF16 35, 16, 16, 5, 2, tc::kPrecBF16

@@ -608,13 +608,17 @@ def test_sampled_parity_at_full_size(name, precision):
     np.testing.assert_allclose(got["importance"].sum(axis=1), 1.0, atol=1e-4)
 
 
-@pytest.mark.parametrize("name,precision", [("hr", "bf16"), ("hr", "tf32x3"), ("bls", "bf16"),
-                                            ("adult", "tf32"), ("wide", "bf16"), ("wide", "tf32x3")])
+@pytest.mark.parametrize("name,precision", [("hr", "bf16"), ("hr", "tf32"), ("hr", "tf32x3"), ("bls", "bf16"),
+                                            ("adult", "bf16"), ("adult", "tf32"), ("adult", "tf32x3"),
+                                            ("wide", "bf16"), ("wide", "tf32x3")])
 def test_row_partition_geometry_bitwise(name, precision):
     """Every batch size maps rows to CTAs, tiles and warps differently (equal
     contiguous row blocks per CTA, partial last tiles, warps without rows):
     the outputs of each row must not depend on it.  Odd sizes around the tile,
-    warp and per-CTA boundaries, on the device path, against 1,000-row calls."""
+    warp and per-CTA boundaries, on the device path, against 1,000-row calls.
+    The 1,000-row calls and batches up to 2 tiles per CTA run K2's latency
+    instance (2 row groups), larger and packed batches the throughput instance
+    (up to 4): the two must agree bit for bit."""
     import torch
     from paper_2510_19689_b200.device import DeviceRunner
     m = P.TabNetModel.from_reference(W.make_model(name), precision=precision)

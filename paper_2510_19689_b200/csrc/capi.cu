@@ -377,9 +377,13 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
 }  // extern "C"
 
 // ------------------------- host-buffer path -------------------------------
-// Reference-facing synchronous call with HOST buffers.  The batch is cut into
-// row chunks that flow through kNumStreams streams, so chunk i's H2D, chunk
-// i-1's kernel and chunk i-2's D2H overlap (PCIe is full duplex).  Page-locked
+// Reference-facing synchronous call with HOST buffers.  Batches up to
+// kZeroCopyMax rows (kZeroCopyMaxStaged through the staging) run as ONE kernel
+// that reads x from and writes the outputs straight into page-locked host
+// memory over PCIe (zero-copy: no per-array DMA set-up, the latency path).
+// Larger batches are cut into row chunks that flow through kNumStreams
+// streams, so chunk i's H2D, chunk i-1's kernel and chunk i-2's D2H overlap
+// (PCIe is full duplex).  Page-locked
 // caller buffers (cudaHostAlloc / torch pin_memory) are DMA'd directly; other
 // buffers (and the float64 numpy path) are staged through per-stream pinned
 // memory with the f64<->f32 conversion fused into the staging copy.
@@ -392,6 +396,14 @@ constexpr int64_t kMinChunk = 8192;
 // vs 70 / 72 us with one DMA per output array; even at 256; the host copy-out
 // loses above (512 rows: 87-90 vs 77 us)
 constexpr int64_t kSmallBatch = 128;
+// zero-copy up to here: HR end-to-end 2,048 / 8,192 / 32,768 rows 79 / 180 /
+// 633 us vs 117 / 253 / 666 us through copy-engine transfers; at 65,536 rows
+// the copy engines win (1.22 vs 1.25 ms)
+constexpr int64_t kZeroCopyMax = 32768;
+// through the staging (float64 apply): HR 8,192 rows 0.66 vs 1.45 ms; above
+// 2 * kMinChunk the chunked pipeline overlaps the host conversions with the
+// transfers and wins (32,768 rows: 0.95 vs 1.55 ms)
+constexpr int64_t kZeroCopyMaxStaged = 2 * kMinChunk;
 
 struct StreamCtx {
   cudaStream_t stream = nullptr;
@@ -498,6 +510,18 @@ cudaError_t ensure(StreamCtx* c, size_t pin_bytes, size_t dev_bytes) {
   return cudaSuccess;
 }
 
+// the device-side address of page-locked host memory (the same address under
+// unified addressing); nullptr for null or unmapped pointers
+void* mapped(const void* p) {
+  if (!p) return nullptr;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, const_cast<void*>(p), 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return d;
+}
+
 bool is_pinned(const void* p) {
   if (!p) return true;
   cudaPointerAttributes at{};
@@ -578,14 +602,25 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     o.predicted_class = nullptr;
   }
   constexpr bool kF32 = sizeof(T) == 4;
-  // Small batches (the serving/latency path) always go through the pinned
-  // staging: 3 API calls (H2D, kernel, D2H) beat one DMA per output array.
-  const bool small = rows <= kSmallBatch;
-  const bool direct = !small && kF32 && is_pinned(x) && is_pinned(o.logits) && is_pinned(o.probabilities) &&
-                      is_pinned(o.masks) && is_pinned(o.importance) && is_pinned(o.predicted_class);
+  const bool pinned_all = kF32 && is_pinned(x) && is_pinned(o.logits) && is_pinned(o.probabilities) &&
+                          is_pinned(o.masks) && is_pinned(o.importance) && is_pinned(o.predicted_class);
+  // Up to kZeroCopyMax rows the kernel itself reads x from and writes the
+  // outputs into page-locked host memory (the caller's, or the staging) over
+  // PCIe: no copy-engine transfers.  Small batches without page-locked caller
+  // buffers go through the staging as one cached graph.
+  // (caller buffers registered without a device mapping take the copy path)
+  auto all_mapped = [&]() {
+    const void* ps[] = {x, o.logits, o.probabilities, o.masks, o.importance, o.predicted_class};
+    for (const void* q : ps)
+      if (q && !mapped(q)) return false;
+    return true;
+  };
+  const bool zc = pinned_all ? rows <= kZeroCopyMax && all_mapped() : rows <= kZeroCopyMaxStaged;
+  const bool small = rows <= kSmallBatch && !(zc && pinned_all);
+  const bool direct = !small && pinned_all;
   // Batch statistics (negative control) need the whole batch in one call.
   int64_t chunk = rows;
-  if (!(flags & TBN_FLAG_BATCH_STATS) && rows > 2 * kMinChunk) {
+  if (!zc && !(flags & TBN_FLAG_BATCH_STATS) && rows > 2 * kMinChunk) {
     chunk = (rows + kNumStreams - 1) / kNumStreams;
     chunk = ((chunk + 127) / 128) * 128;
     if (chunk < kMinChunk) chunk = kMinChunk;
@@ -632,6 +667,84 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     char* P = (char*)sc.pin;
     char* D = (char*)sc.dev;
     cudaStream_t cs = sc.stream;
+    if (zc) {
+      // one chunk: the kernel reads/writes host memory through its device mapping
+      const float* hx;
+      tbn_outputs hout{};
+      if (direct) {
+        hx = (const float*)(const void*)x;
+        hout.logits = (float*)(void*)o.logits;
+        hout.probabilities = (float*)(void*)o.probabilities;
+        hout.masks = (float*)(void*)o.masks;
+        hout.importance = (float*)(void*)o.importance;
+        hout.predicted_class = o.predicted_class;
+      } else {
+        convert_all(std::vector<ConvertJob<float, T>>{{(float*)(P + L.x), x, n * F}});
+        hx = (const float*)(P + L.x);
+        hout.logits = o.logits ? (float*)(P + L.logits) : nullptr;
+        hout.probabilities = o.probabilities ? (float*)(P + L.probs) : nullptr;
+        hout.masks = o.masks ? (float*)(P + L.masks) : nullptr;
+        hout.importance = o.importance ? (float*)(P + L.imp) : nullptr;
+        hout.predicted_class = o.predicted_class ? (int32_t*)(P + L.pred) : nullptr;
+      }
+      tbn_outputs dout{};
+      const float* dx = (const float*)mapped(hx);
+      dout.logits = (float*)mapped(hout.logits);
+      dout.probabilities = (float*)mapped(hout.probabilities);
+      dout.masks = (float*)mapped(hout.masks);
+      dout.importance = (float*)mapped(hout.importance);
+      dout.predicted_class = (int32_t*)mapped(hout.predicted_class);
+      if (!dx || (hout.logits && !dout.logits) || (hout.probabilities && !dout.probabilities) ||
+          (hout.masks && !dout.masks) || (hout.importance && !dout.importance) ||
+          (hout.predicted_class && !dout.predicted_class))
+        return fail(TBN_ERR_CUDA, "host buffer not mapped into the device address space");
+      auto enqueue = [&]() -> tbn_status {
+        TBN_CUDA(cudaMemsetAsync(D + L.err, 0, 4, cs));
+        tbn_status s2 = tbn_forward(m, dx, n, flags, &dout, (int32_t*)(D + L.err), D + L.ws, L.total - L.ws, cs);
+        if (s2 != TBN_OK) return s2;
+        TBN_CUDA(cudaMemcpyAsync(P + err_off, D + L.err, 4, cudaMemcpyDeviceToHost, cs));
+        return TBN_OK;
+      };
+      static const bool no_graphs_zc = getenv("TBN_TRACE") || getenv("TBN_TRACE_MAPPED");
+      if (!direct && rows <= kSmallBatch && !no_graphs_zc) {
+        // staging (stable pointers): [err memset, forward, err D2H] as one cached CUDA graph
+        const uint32_t omask = (o.logits ? 1u : 0u) | (o.probabilities ? 2u : 0u) | (o.masks ? 4u : 0u) |
+                               (o.importance ? 8u : 0u) | (o.predicted_class ? 16u : 0u);
+        cudaGraphExec_t exec = nullptr;
+        for (const SmallGraph& sg : hc->graphs)
+          if (sg.model_id == m->id && sg.rows == n && sg.flags == flags && sg.omask == omask && sg.pin == sc.pin &&
+              sg.dev == sc.dev) {
+            exec = sg.exec;
+            break;
+          }
+        if (!exec) {
+          TBN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+          st = enqueue();
+          cudaGraph_t graph = nullptr;
+          const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+          if (st != TBN_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+          }
+          if (ce != cudaSuccess) return cuda_fail(ce, "small-batch graph capture");
+          const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+          cudaGraphDestroy(graph);
+          if (ie != cudaSuccess) return cuda_fail(ie, "small-batch graph instantiate");
+          if (hc->graphs.size() >= kMaxGraphs) {
+            cudaGraphExecDestroy(hc->graphs.front().exec);
+            hc->graphs.erase(hc->graphs.begin());
+          }
+          hc->graphs.push_back({m->id, n, flags, omask, sc.pin, sc.dev, exec});
+        }
+        TBN_CUDA(cudaGraphLaunch(exec, cs));
+      } else {
+        st = enqueue();
+        if (st != TBN_OK) return st;
+      }
+      sc.pending_r0 = r0;
+      sc.pending_rows = n;
+      continue;
+    }
     if (direct) {
       TBN_CUDA(cudaMemsetAsync(D + L.err, 0, 4, cs));
       TBN_CUDA(cudaMemcpyAsync(D + L.x, (const float*)x + r0 * F, n * F * 4, cudaMemcpyHostToDevice, cs));

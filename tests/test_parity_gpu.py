@@ -646,15 +646,16 @@ def test_row_partition_geometry_bitwise(name, precision):
 
 @pytest.mark.parametrize("precision", ["bf16", "tf32x3"])
 def test_host_call_pinned_buffers_graph_replay(precision):
-    """tbn_forward_host with pinned caller buffers (the DMA-direct path, chunked
-    over 3 streams from 16,384 rows): repeated calls with new contents in the same
+    """tbn_forward_host with pinned caller buffers: up to 32,768 rows the kernel
+    reads and writes them directly (zero-copy), above it the DMA-direct path
+    chunked over 3 streams.  Repeated calls with new contents in the same
     buffers must equal the device path bitwise; non-finite input still raises."""
     import torch
     from paper_2510_19689_b200.device import DeviceRunner
     m = P.TabNetModel.from_reference(W.make_model("hr"), precision=precision)
     eng = m.engine()
-    runner = DeviceRunner(m, max_rows=20000)
-    for rows in (33, 1000, 8192, 20000):
+    runner = DeviceRunner(m, max_rows=40000)
+    for rows in (1, 33, 1000, 8192, 20000, 40000):
         xp = torch.empty((rows, 35), dtype=torch.float32).pin_memory()
         outs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in runner.views(rows).items()}
         npo = {k: v.numpy() for k, v in outs.items()}
@@ -668,6 +669,29 @@ def test_host_call_pinned_buffers_graph_replay(precision):
         xp[rows // 2, 3] = float("nan")
         with pytest.raises(P.InvalidInputError):
             eng.forward_host_f32(xp.numpy(), 0, npo)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32x3"])
+def test_apply_f64_host_paths_bitwise(precision):
+    """The float64 apply() host paths: the cached small-batch graph (<= 128
+    rows), the zero-copy staging (<= 16,384 rows) and the chunked pipeline
+    above: each must return exactly the device path's fp32 outputs as float64,
+    including after the result buffers are recycled."""
+    import torch
+    from paper_2510_19689_b200.device import DeviceRunner
+    m = P.TabNetModel.from_reference(W.make_model("hr"), precision=precision)
+    runner = DeviceRunner(m, max_rows=40000)
+    for rows in (1, 128, 129, 16384, 16385, 40000):
+        for seed in (5, 6):
+            x = W.make_inputs(W.WORKLOADS["hr"], rows, seed=seed)
+            r = m.apply(x.astype(np.float64))
+            ref = runner.run(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            for k in ("logits", "probabilities", "masks", "importance"):
+                got = getattr(r, k)
+                assert got.dtype == np.float64
+                assert np.array_equal(got, ref[k].cpu().numpy().astype(np.float64)), (rows, seed, k)
+            del r
 
 
 def _emu_stats(got, emu):

@@ -1,7 +1,9 @@
-# e2e A/B: copy-engine chunks vs the kernel reading/writing the caller's pinned buffers (TBN_ZERO_COPY)
-for c in hr bls adult; do for z in 0 1; do
-  if [ $z = 1 ]; then export TBN_ZERO_COPY=1; else unset TBN_ZERO_COPY; fi
-  python bench.py --config $c --no-cpu-baseline --no-parity-mode --steps 10 > gpurun_out/zc.json 2>/dev/null
-  python -c "import json; d=json.load(open('gpurun_out/zc.json')); e=d['e2e']; print('$c zc=$z', round(e['ms_per_step'],4), 'ms', '%.3g'%e['value'], 'device', round(d['ms_per_step']*1000,1), 'us')"
-done; done
-TBN_ZERO_COPY=1 python -m pytest tests/test_parity_gpu.py -q -m gpu -k "pinned_buffers" 2>&1 | tail -2
+# e2e with zero-copy up to kZeroCopyMax rows: latency sweep (1..1,024 rows), larger batches, float64 apply
+python bench.py --config hr_latency --rows 1024 --latency-sweep --no-cpu-baseline --no-parity-mode --no-e2e --steps 5 > gpurun_out/zc.json 2>/dev/null
+python -c "
+import json; d=json.load(open('gpurun_out/zc.json'))
+print('lat', {k: round(v['e2e_p50']*1000,1) for k,v in d['latency_sweep'].items()})"
+for r in 2048 8192 32768 65536; do
+  python bench.py --config hr --rows $r --no-cpu-baseline --no-parity-mode --inflight 0 --steps 10 > gpurun_out/zc.json 2>/dev/null
+  python -c "import json; d=json.load(open('gpurun_out/zc.json')); e=d['e2e']; print('rows=$r', round(e['ms_per_step']*1000,1), 'us; apply_f64', round(e['apply_f64']['ms_per_call']*1000,1), 'us')"
+done

@@ -169,7 +169,16 @@ def crc32c(data: bytes, crc: int = 0) -> int:
 
 
 def ptr(a: np.ndarray | None) -> int | None:
-    return None if a is None else a.ctypes.data
+    """Data pointer of an array.  ``ctypes.c_char.from_buffer`` is ~5x cheaper
+    than ``a.ctypes.data`` (which builds a ctypes helper object per call) and
+    matters on the latency path; read-only, empty or non-contiguous arrays take
+    the general route."""
+    if a is None:
+        return None
+    try:
+        return C.addressof(C.c_char.from_buffer(a))
+    except (TypeError, ValueError, BufferError):
+        return a.ctypes.data
 
 
 def env_device() -> int:

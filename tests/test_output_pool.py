@@ -83,3 +83,15 @@ def test_concurrent_take_and_release():
     for t in ts:
         t.join()
     assert not errs
+
+
+def test_native_ptr_matches_ctypes_data():
+    """_native.ptr (the latency path's cheap data pointer) equals
+    ndarray.ctypes.data for writable, read-only, empty and strided arrays."""
+    from paper_2510_19689_b200 import _native as N
+    a = np.empty((5, 3, 35), np.float32)
+    ro = a.copy()
+    ro.setflags(write=False)
+    for arr in (a, ro, np.empty((0, 35), np.float32), a[:, ::2], np.empty(7, np.int32)):
+        assert N.ptr(arr) == arr.ctypes.data
+    assert N.ptr(None) is None

@@ -132,8 +132,10 @@ size_t tbn_workspace_bytes(const tbn_model* model, int64_t rows, uint32_t flags)
  * transformers, S attentive steps with sparsemax, head/softmax, importance.
  * Async forward on `stream` (a cudaStream_t; NULL = legacy default stream).
  * x: device float32 (rows, F) row-major.  Outputs are device pointers.
- * A non-finite input sets *err_flag (device int32, may be NULL) to nonzero;
- * the caller checks it after synchronizing (tbn_forward_host does).
+ * A non-finite input sets *err_flag (int32, may be NULL) to 1 with a plain
+ * store; the caller zeroes it before and checks it after synchronizing
+ * (tbn_forward_host does).  It may point to device memory or to device-mapped
+ * page-locked host memory.
  * Per-row results are bitwise independent of `rows`, tile position, grid size
  * and concurrency (invariance.py:56-82). */
 tbn_status tbn_forward(const tbn_model* model, const float* x, int64_t rows,

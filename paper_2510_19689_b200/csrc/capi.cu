@@ -379,23 +379,19 @@ tbn_status tbn_forward(const tbn_model* m, const float* x, int64_t rows, uint32_
 // ------------------------- host-buffer path -------------------------------
 // Reference-facing synchronous call with HOST buffers.  Batches up to
 // kZeroCopyMax rows (kZeroCopyMaxStaged through the staging) run as ONE kernel
-// that reads x from and writes the outputs straight into page-locked host
-// memory over PCIe (zero-copy: no per-array DMA set-up, the latency path).
-// Larger batches are cut into row chunks that flow through kNumStreams
-// streams, so chunk i's H2D, chunk i-1's kernel and chunk i-2's D2H overlap
-// (PCIe is full duplex).  Page-locked
-// caller buffers (cudaHostAlloc / torch pin_memory) are DMA'd directly; other
-// buffers (and the float64 numpy path) are staged through per-stream pinned
-// memory with the f64<->f32 conversion fused into the staging copy.
+// that reads x from and writes the outputs and the error flag straight into
+// page-locked host memory over PCIe (zero-copy: one launch and one
+// synchronize, the latency path).  Larger batches are cut into row chunks that
+// flow through kNumStreams streams, so chunk i's H2D, chunk i-1's kernel and
+// chunk i-2's D2H overlap (PCIe is full duplex).  Page-locked caller buffers
+// (cudaHostAlloc / torch pin_memory) are used in place; other buffers (and the
+// float64 numpy path) are staged through per-stream pinned memory with the
+// f64<->f32 conversion fused into the staging copy.
 // Per-row results are bitwise independent of the chunking (invariance contract).
 namespace {
 
 constexpr int kNumStreams = 3;
 constexpr int64_t kMinChunk = 8192;
-// staged + graph path up to here: HR end-to-end p50 at 64 / 128 rows 50 / 54 us
-// vs 70 / 72 us with one DMA per output array; even at 256; the host copy-out
-// loses above (512 rows: 87-90 vs 77 us)
-constexpr int64_t kSmallBatch = 128;
 // zero-copy up to here: HR end-to-end 2,048 / 8,192 / 32,768 rows 79 / 180 /
 // 633 us vs 117 / 253 / 666 us through copy-engine transfers; at 65,536 rows
 // the copy engines win (1.22 vs 1.25 ms)
@@ -412,22 +408,9 @@ struct StreamCtx {
   int64_t pending_r0 = -1, pending_rows = 0;   // chunk whose staged outputs await copy-out
 };
 
-// A small batch's [H2D, forward, D2H] sequence captured once as a CUDA graph
-// and replayed (one launch instead of three API calls on the serving path).
-struct SmallGraph {
-  uint64_t model_id;
-  int64_t rows;
-  uint32_t flags, omask;
-  void* pin;
-  void* dev;
-  cudaGraphExec_t exec;
-};
-
 struct HostCtx {
   StreamCtx s[kNumStreams];
-  std::vector<SmallGraph> graphs;     // LRU-ish, capped (kMaxGraphs)
 };
-constexpr size_t kMaxGraphs = 128;
 
 void free_host_ctx(int device, HostCtx* c) {
   if (cudaSetDevice(device) != cudaSuccess) {   // runtime already torn down: nothing to free
@@ -436,7 +419,6 @@ void free_host_ctx(int device, HostCtx* c) {
   }
   for (auto& sc : c->s)
     if (sc.stream) cudaStreamSynchronize(sc.stream);
-  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   for (auto& sc : c->s) {
     if (sc.pin) cudaFreeHost(sc.pin);
     if (sc.dev) cudaFree(sc.dev);
@@ -604,11 +586,10 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   constexpr bool kF32 = sizeof(T) == 4;
   const bool pinned_all = kF32 && is_pinned(x) && is_pinned(o.logits) && is_pinned(o.probabilities) &&
                           is_pinned(o.masks) && is_pinned(o.importance) && is_pinned(o.predicted_class);
-  // Up to kZeroCopyMax rows the kernel itself reads x from and writes the
-  // outputs into page-locked host memory (the caller's, or the staging) over
-  // PCIe: no copy-engine transfers.  Small batches without page-locked caller
-  // buffers go through the staging as one cached graph.
-  // (caller buffers registered without a device mapping take the copy path)
+  // Up to kZeroCopyMax rows (kZeroCopyMaxStaged through the staging) the kernel
+  // itself reads x from and writes the outputs and the error flag into
+  // page-locked host memory over PCIe: one launch, no copy-engine transfers.
+  // Caller buffers registered without a device mapping take the copy path.
   auto all_mapped = [&]() {
     const void* ps[] = {x, o.logits, o.probabilities, o.masks, o.importance, o.predicted_class};
     for (const void* q : ps)
@@ -616,8 +597,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     return true;
   };
   const bool zc = pinned_all ? rows <= kZeroCopyMax && all_mapped() : rows <= kZeroCopyMaxStaged;
-  const bool small = rows <= kSmallBatch && !(zc && pinned_all);
-  const bool direct = !small && pinned_all;
+  const bool direct = pinned_all;              // outputs land in the caller's buffers (DMA or zero-copy)
   // Batch statistics (negative control) need the whole batch in one call.
   int64_t chunk = rows;
   if (!zc && !(flags & TBN_FLAG_BATCH_STATS) && rows > 2 * kMinChunk) {
@@ -641,7 +621,7 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     TBN_CUDA(cudaStreamSynchronize(sc.stream));
     char* P = (char*)sc.pin;
     const size_t r0 = sc.pending_r0, n = sc.pending_rows;
-    err_any |= *(int32_t*)(P + err_off);
+    err_any |= *(volatile int32_t*)(P + err_off);
     if (!direct) {
       using OutF = std::remove_pointer_t<decltype(o.logits)>;
       std::vector<ConvertJob<OutF, float>> jobs;
@@ -687,60 +667,22 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
         hout.importance = o.importance ? (float*)(P + L.imp) : nullptr;
         hout.predicted_class = o.predicted_class ? (int32_t*)(P + L.pred) : nullptr;
       }
+      int32_t* herr = (int32_t*)(P + err_off);
+      *(volatile int32_t*)herr = 0;               // the previous call on this stream has finished
       tbn_outputs dout{};
       const float* dx = (const float*)mapped(hx);
+      int32_t* derr = (int32_t*)mapped(herr);
       dout.logits = (float*)mapped(hout.logits);
       dout.probabilities = (float*)mapped(hout.probabilities);
       dout.masks = (float*)mapped(hout.masks);
       dout.importance = (float*)mapped(hout.importance);
       dout.predicted_class = (int32_t*)mapped(hout.predicted_class);
-      if (!dx || (hout.logits && !dout.logits) || (hout.probabilities && !dout.probabilities) ||
+      if (!dx || !derr || (hout.logits && !dout.logits) || (hout.probabilities && !dout.probabilities) ||
           (hout.masks && !dout.masks) || (hout.importance && !dout.importance) ||
           (hout.predicted_class && !dout.predicted_class))
         return fail(TBN_ERR_CUDA, "host buffer not mapped into the device address space");
-      auto enqueue = [&]() -> tbn_status {
-        TBN_CUDA(cudaMemsetAsync(D + L.err, 0, 4, cs));
-        tbn_status s2 = tbn_forward(m, dx, n, flags, &dout, (int32_t*)(D + L.err), D + L.ws, L.total - L.ws, cs);
-        if (s2 != TBN_OK) return s2;
-        TBN_CUDA(cudaMemcpyAsync(P + err_off, D + L.err, 4, cudaMemcpyDeviceToHost, cs));
-        return TBN_OK;
-      };
-      static const bool no_graphs_zc = getenv("TBN_TRACE") || getenv("TBN_TRACE_MAPPED");
-      if (!direct && rows <= kSmallBatch && !no_graphs_zc) {
-        // staging (stable pointers): [err memset, forward, err D2H] as one cached CUDA graph
-        const uint32_t omask = (o.logits ? 1u : 0u) | (o.probabilities ? 2u : 0u) | (o.masks ? 4u : 0u) |
-                               (o.importance ? 8u : 0u) | (o.predicted_class ? 16u : 0u);
-        cudaGraphExec_t exec = nullptr;
-        for (const SmallGraph& sg : hc->graphs)
-          if (sg.model_id == m->id && sg.rows == n && sg.flags == flags && sg.omask == omask && sg.pin == sc.pin &&
-              sg.dev == sc.dev) {
-            exec = sg.exec;
-            break;
-          }
-        if (!exec) {
-          TBN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-          st = enqueue();
-          cudaGraph_t graph = nullptr;
-          const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-          if (st != TBN_OK) {
-            if (graph) cudaGraphDestroy(graph);
-            return st;
-          }
-          if (ce != cudaSuccess) return cuda_fail(ce, "small-batch graph capture");
-          const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
-          cudaGraphDestroy(graph);
-          if (ie != cudaSuccess) return cuda_fail(ie, "small-batch graph instantiate");
-          if (hc->graphs.size() >= kMaxGraphs) {
-            cudaGraphExecDestroy(hc->graphs.front().exec);
-            hc->graphs.erase(hc->graphs.begin());
-          }
-          hc->graphs.push_back({m->id, n, flags, omask, sc.pin, sc.dev, exec});
-        }
-        TBN_CUDA(cudaGraphLaunch(exec, cs));
-      } else {
-        st = enqueue();
-        if (st != TBN_OK) return st;
-      }
+      st = tbn_forward(m, dx, n, flags, &dout, derr, D + L.ws, L.total - L.ws, cs);
+      if (st != TBN_OK) return st;
       sc.pending_r0 = r0;
       sc.pending_rows = n;
       continue;
@@ -750,7 +692,8 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
       TBN_CUDA(cudaMemcpyAsync(D + L.x, (const float*)x + r0 * F, n * F * 4, cudaMemcpyHostToDevice, cs));
     } else {
       convert_all(std::vector<ConvertJob<float, T>>{{(float*)(P + L.x), x + r0 * F, n * F}});
-      *(int32_t*)(P + L.err) = 0;                 // [x | err] in one copy (issued below)
+      *(int32_t*)(P + L.err) = 0;                 // [x | err] in one copy
+      TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, L.err + 4 - L.x, cudaMemcpyHostToDevice, cs));
     }
     tbn_outputs dout{};
     dout.logits = o.logits ? (float*)(D + L.logits) : nullptr;
@@ -758,46 +701,6 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
     dout.masks = o.masks ? (float*)(D + L.masks) : nullptr;
     dout.importance = o.importance ? (float*)(D + L.imp) : nullptr;
     dout.predicted_class = o.predicted_class ? (int32_t*)(D + L.pred) : nullptr;
-    static const bool no_graphs = getenv("TBN_TRACE") || getenv("TBN_TRACE_MAPPED");
-    if (small && !no_graphs) {
-      // [x|err] H2D, forward, [err|outputs] D2H as one cached CUDA graph
-      const uint32_t omask = (o.logits ? 1u : 0u) | (o.probabilities ? 2u : 0u) | (o.masks ? 4u : 0u) |
-                             (o.importance ? 8u : 0u) | (o.predicted_class ? 16u : 0u);
-      cudaGraphExec_t exec = nullptr;
-      for (const SmallGraph& sg : hc->graphs)
-        if (sg.model_id == m->id && sg.rows == n && sg.flags == flags && sg.omask == omask &&
-            sg.pin == sc.pin && sg.dev == sc.dev) {
-          exec = sg.exec;
-          break;
-        }
-      if (!exec) {
-        TBN_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        cudaMemcpyAsync(D + L.x, P + L.x, L.err + 4 - L.x, cudaMemcpyHostToDevice, cs);
-        st = tbn_forward(m, (const float*)(D + L.x), n, flags, &dout, (int32_t*)(D + L.err),
-                         D + L.ws, L.total - L.ws, cs);
-        cudaMemcpyAsync(P + L.err, D + L.err, L.pred + n * 4 - L.err, cudaMemcpyDeviceToHost, cs);
-        cudaGraph_t graph = nullptr;
-        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-        if (st != TBN_OK) {
-          if (graph) cudaGraphDestroy(graph);
-          return st;
-        }
-        if (ce != cudaSuccess) return cuda_fail(ce, "small-batch graph capture");
-        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (ie != cudaSuccess) return cuda_fail(ie, "small-batch graph instantiate");
-        if (hc->graphs.size() >= kMaxGraphs) {
-          cudaGraphExecDestroy(hc->graphs.front().exec);
-          hc->graphs.erase(hc->graphs.begin());
-        }
-        hc->graphs.push_back({m->id, n, flags, omask, sc.pin, sc.dev, exec});
-      }
-      TBN_CUDA(cudaGraphLaunch(exec, cs));
-      sc.pending_r0 = r0;
-      sc.pending_rows = n;
-      continue;
-    }
-    if (!direct) TBN_CUDA(cudaMemcpyAsync(D + L.x, P + L.x, L.err + 4 - L.x, cudaMemcpyHostToDevice, cs));
     st = tbn_forward(m, (const float*)(D + L.x), n, flags, &dout, (int32_t*)(D + L.err),
                      D + L.ws, L.total - L.ws, cs);
     if (st != TBN_OK) return st;
@@ -811,9 +714,6 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
       if ((fo = (float*)(void*)o.importance)) TBN_CUDA(cudaMemcpyAsync(fo + r0 * F, dout.importance, n * F * 4, cudaMemcpyDeviceToHost, cs));
       if (o.predicted_class) TBN_CUDA(cudaMemcpyAsync(o.predicted_class + r0, dout.predicted_class, n * 4, cudaMemcpyDeviceToHost, cs));
       TBN_CUDA(cudaMemcpyAsync(P + err_off, D + L.err, 4, cudaMemcpyDeviceToHost, cs));
-    } else if (small) {
-      // [err | logits | probs | masks | importance | pred] in one copy
-      TBN_CUDA(cudaMemcpyAsync(P + L.err, D + L.err, L.pred + n * 4 - L.err, cudaMemcpyDeviceToHost, cs));
     } else {
       if (dout.logits) TBN_CUDA(cudaMemcpyAsync(P + L.logits, dout.logits, n * C * 4, cudaMemcpyDeviceToHost, cs));
       if (dout.probabilities) TBN_CUDA(cudaMemcpyAsync(P + L.probs, dout.probabilities, n * C * 4, cudaMemcpyDeviceToHost, cs));

@@ -616,7 +616,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         }
         if constexpr (F % 2) xv[F - 1] = (xv[F - 1] - cst[CF::C_SHIFT + F - 1]) * cst[CF::C_SCALE + F - 1];
       }
-      if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
+      if (valid && bad && a.err_flag) raise_flag(a.err_flag);
       __syncwarp();
 #pragma unroll
       for (int f = 0; f < F; ++f) {

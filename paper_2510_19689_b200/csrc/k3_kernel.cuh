@@ -551,7 +551,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
         tmem_store_n<16>(tq + T_A + (c * FS + o) / 2, pk);
         st32h(my_xn + (o / 8) * 1024, xv, pol);
       }
-      if (bad && a.err_flag) atomicOr(a.err_flag, 1);
+      if (bad && a.err_flag) raise_flag(a.err_flag);
     }
 #pragma unroll
     for (int k = 0; k < C; ++k) lacc[k] = 0.0f;

@@ -574,7 +574,7 @@ tabnet_wide_x3(const Params p, const ForwardArgs a) {
         }
         st32s(at(my_xn, o), xv);
       }
-      if (bad && a.err_flag) atomicOr(a.err_flag, 1);
+      if (bad && a.err_flag) raise_flag(a.err_flag);
     }
     if (c < 2)
       for (int k = 0; k < C; ++k) lacc[k] = 0.0f;

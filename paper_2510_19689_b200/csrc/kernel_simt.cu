@@ -105,7 +105,7 @@ tabnet_forward_simt(SimtParams p, ForwardArgs a) {
       agg[f] = 0.0f;
       msum[f] = 0.0f;
     }
-    if (__any_sync(kFull, bad) && lane == 0 && a.err_flag) atomicOr(a.err_flag, 1);
+    if (__any_sync(kFull, bad) && lane == 0 && a.err_flag) raise_flag(a.err_flag);
     for (int j = lane; j < ND; j += 32) dsum[j] = 0.0f;
     __syncwarp();
     // -- step 0 transformer; a = f0[:, n_d:] (network.py:226-227) --
@@ -411,7 +411,7 @@ tabnet_forward_simt_blk(SimtParams p, ForwardArgs a) {
       r[L.msum + f] = 0.0f;
       r[L.in + f] = 0.0f;
     }
-    if (__any_sync(kFull, bad) && lane == 0 && a.err_flag) atomicOr(a.err_flag, 1);
+    if (__any_sync(kFull, bad) && lane == 0 && a.err_flag) raise_flag(a.err_flag);
     for (int j = lane; j < ND; j += 32) r[L.dsum + j] = 0.0f;
     __syncthreads();
     blk_transform(p, smem, L, L.xn, 0, r, lane);
@@ -558,7 +558,7 @@ __global__ void sparsemax_rows_kernel(const float* __restrict__ z, int64_t rows,
       zs[i] = v;
       zmax = fmaxf(zmax, v);
     }
-    if (__any_sync(kFull, bad) && lane == 0 && err_flag) atomicOr(err_flag, 1);
+    if (__any_sync(kFull, bad) && lane == 0 && err_flag) raise_flag(err_flag);
     zmax = warp_max(zmax);
 #pragma unroll
     for (int i = 0; i < kFPerLane; ++i) zs[i] -= zmax;
@@ -604,7 +604,7 @@ __global__ void sparsemax_rows_f64_kernel(const double* __restrict__ z, int64_t 
       zsum += v;
     }
     if (__any_sync(0xffffffffu, bad)) {
-      if (lane == 0 && err_flag) atomicOr(err_flag, 1);
+      if (lane == 0 && err_flag) raise_flag(err_flag);
       continue;
     }
     zmax = warp_max_d(zmax);                                   // sparsemax.py:32

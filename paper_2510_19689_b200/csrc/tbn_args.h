@@ -23,4 +23,11 @@ struct ForwardArgs {
   int packed;                  // TBN_FLAG_PACKED: host-side launch geometry only
 };
 
+// Raise the non-finite-input flag.  A plain (idempotent) store, not an
+// atomic: the flag may live in device-mapped page-locked host memory (the
+// zero-copy host path), where PCIe atomics are not guaranteed.
+#ifdef __CUDACC__
+__device__ __forceinline__ void raise_flag(int32_t* f) { *(volatile int32_t*)f = 1; }
+#endif
+
 }  // namespace tbn

@@ -740,7 +740,7 @@ tabnet_fused_tc(const TcParams p, const ForwardArgs a) {
         } else {
           xn_half(std::integral_constant<int, 1>{});
         }
-        if (valid && bad && a.err_flag) atomicOr(a.err_flag, 1);
+        if (valid && bad && a.err_flag) raise_flag(a.err_flag);
       }
       if (trt) TBN_TRACE(3092);
       float prev[HH];

@@ -7,13 +7,40 @@
 // reference-facing Python apply() and bench.py's e2e leg use.
 #include "tabnet_b200.h"
 #include "tbn_internal.h"
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <thread>
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX3: free when no profiler is attached
 
 namespace {
 // NVTX range for nsys/ncu timelines: forward, H2D, D2H of the host path
+// TBN_HOST_TIMING=<ms>: report host-path phases slower than that to stderr
+// (development aid for latency tails; off by default)
+double host_timing_ms() {
+  static const double v = [] {
+    const char* e = std::getenv("TBN_HOST_TIMING");
+    return e ? std::atof(e) : -1.0;
+  }();
+  return v;
+}
 struct NvtxRange {
-  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-  ~NvtxRange() { nvtxRangePop(); }
+  explicit NvtxRange(const char* name) : name_(name) {
+    nvtxRangePushA(name);
+    if (host_timing_ms() >= 0) t0_ = std::chrono::steady_clock::now();
+  }
+  ~NvtxRange() {
+    nvtxRangePop();
+    if (host_timing_ms() >= 0) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+      if (ms >= host_timing_ms())
+        std::fprintf(stderr, "[tbn host] %s: %.3f ms (thread %zu)\n", name_, ms,
+                     std::hash<std::thread::id>()(std::this_thread::get_id()) % 100000);
+    }
+  }
+  const char* name_;
+  std::chrono::steady_clock::time_point t0_;
   NvtxRange(const NvtxRange&) = delete;
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
@@ -428,31 +455,60 @@ void free_host_ctx(int device, HostCtx* c) {
   delete c;
 }
 
-// Per-thread owner of the host-path contexts: released when the thread exits
-// (the reference's invariance.py:40-41 spins up a fresh 32-thread pool per
-// call, so leaking them would grow pinned + device memory without bound).
-struct HostCtxOwner {
-  std::map<int, HostCtx*> ctxs;
-  ~HostCtxOwner() {
-    for (auto& kv : ctxs) free_host_ctx(kv.first, kv.second);
-  }
+// Host-path contexts (streams + pinned/device staging) are leased per call
+// from a process-wide pool per device: apply() is reentrant and
+// concurrent callers never share one, but callers' threads come and go (the
+// serving workers of each InferenceService, invariance.py:40-41's fresh
+// 32-thread pool per check) while the contexts and their staging stay
+// allocated and warm.  Creating a context and growing its staging cost
+// 25-330 ms under concurrent traffic (stream creation and cudaFree serialise
+// against other threads' work), which per-thread contexts paid on every new
+// thread.  The pool holds at most the peak number of concurrent calls.
+struct CtxPool {
+  std::mutex mu;
+  std::vector<HostCtx*> free[tbn::kMaxDevices];
 };
+CtxPool& ctx_pool() {
+  static CtxPool* p = new CtxPool();      // never destroyed: calls may run during exit
+  return *p;
+}
 
-HostCtx* host_ctx(int device) {
-  // Per-thread, per-device: apply() is reentrant and 32
-  // concurrent callers (invariance.py:40-41) never share buffers or streams.
-  thread_local HostCtxOwner owner;
-  auto it = owner.ctxs.find(device);
-  if (it != owner.ctxs.end()) return it->second;
+HostCtx* lease_host_ctx(int device) {
+  if (device < 0 || device >= tbn::kMaxDevices) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(ctx_pool().mu);
+    auto& f = ctx_pool().free[device];
+    if (!f.empty()) {
+      HostCtx* c = f.back();
+      f.pop_back();
+      return c;
+    }
+  }
+  NvtxRange nv("tbn_host: context creation");
   HostCtx* c = new HostCtx();
   for (auto& sc : c->s)
     if (cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking) != cudaSuccess) {
       free_host_ctx(device, c);
       return nullptr;
     }
-  owner.ctxs[device] = c;
   return c;
 }
+
+void return_host_ctx(int device, HostCtx* c) {
+  std::lock_guard<std::mutex> lk(ctx_pool().mu);
+  ctx_pool().free[device].push_back(c);
+}
+
+struct CtxLease {
+  int device;
+  HostCtx* hc;
+  explicit CtxLease(int d) : device(d), hc(lease_host_ctx(d)) {}
+  ~CtxLease() {
+    if (hc) return_host_ctx(device, hc);
+  }
+  CtxLease(const CtxLease&) = delete;
+  CtxLease& operator=(const CtxLease&) = delete;
+};
 
 // On any early error return from the host path, wait for the chunks already
 // queued (their DMAs read/write the per-thread pinned staging) before the
@@ -470,24 +526,30 @@ struct DrainOnError {
   }
 };
 
+// Staging grows to the next power of two (at least 1 MB): each reallocation
+// (cudaFreeHost / cudaFree synchronise with the whole device) happens at most
+// log2 times per context.
+size_t staging_size(size_t need) {
+  size_t v = (size_t)1 << 20;
+  while (v < need) v <<= 1;
+  return v;
+}
 cudaError_t ensure(StreamCtx* c, size_t pin_bytes, size_t dev_bytes) {
   if (c->pin_bytes < pin_bytes) {
     if (c->pin) cudaFreeHost(c->pin);
     c->pin = nullptr; c->pin_bytes = 0;
-    cudaError_t e = cudaMallocHost(&c->pin, pin_bytes);
+    const size_t sz = staging_size(pin_bytes);
+    cudaError_t e = cudaMallocHost(&c->pin, sz);
     if (e != cudaSuccess) return e;
-    c->pin_bytes = pin_bytes;
+    c->pin_bytes = sz;
   }
   if (c->dev_bytes < dev_bytes) {
     if (c->dev) cudaFree(c->dev);
     c->dev = nullptr; c->dev_bytes = 0;
-    cudaError_t e = cudaMalloc(&c->dev, dev_bytes);
+    const size_t sz = staging_size(dev_bytes);
+    cudaError_t e = cudaMalloc(&c->dev, sz);
     if (e != cudaSuccess) return e;
-    // defined contents for the alignment gaps the single-copy small-batch path
-    // moves along with the outputs (compute-sanitizer initcheck)
-    e = cudaMemset(c->dev, 0, dev_bytes);
-    if (e != cudaSuccess) return e;
-    c->dev_bytes = dev_bytes;
+    c->dev_bytes = sz;
   }
   return cudaSuccess;
 }
@@ -572,7 +634,8 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   NvtxRange nv("tbn_forward_host");
   if (!x) return fail(TBN_ERR_INVALID_INPUT, "null input");
   DeviceGuard guard(m->device);
-  HostCtx* hc = host_ctx(m->device);
+  CtxLease lease(m->device);
+  HostCtx* hc = lease.hc;
   if (!hc) return fail(TBN_ERR_CUDA, "cannot create streams");
   const size_t F = m->cfg.feature_count, C = m->cfg.n_classes, S = m->cfg.n_steps;
   OutT o{};
@@ -607,10 +670,13 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   }
   const Layout L = layout_for(m, chunk, flags);
   DrainOnError drain_guard{hc};
-  for (auto& sc : hc->s) {
-    if (sc.pending_r0 >= 0) TBN_CUDA(cudaStreamSynchronize(sc.stream));   // (defensive: never left set)
-    sc.pending_r0 = -1;
-    TBN_CUDA(ensure(&sc, direct ? 256 : L.total, L.total));
+  {
+    NvtxRange nv_ensure("tbn_host: staging allocation");
+    for (auto& sc : hc->s) {
+      if (sc.pending_r0 >= 0) TBN_CUDA(cudaStreamSynchronize(sc.stream));   // (defensive: never left set)
+      sc.pending_r0 = -1;
+      TBN_CUDA(ensure(&sc, direct ? 256 : L.total, L.total));
+    }
   }
   int32_t err_any = 0;
   const size_t err_off = direct ? 0 : L.err;   // pinned landing slot of the chunk's error flag
@@ -618,7 +684,10 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   auto drain = [&](StreamCtx& sc) -> tbn_status {
     if (sc.pending_r0 < 0) return TBN_OK;
     NvtxRange nv("tbn_host: D2H wait + output conversion");
-    TBN_CUDA(cudaStreamSynchronize(sc.stream));
+    {
+      NvtxRange nv_sync("tbn_host: stream synchronize");
+      TBN_CUDA(cudaStreamSynchronize(sc.stream));
+    }
     char* P = (char*)sc.pin;
     const size_t r0 = sc.pending_r0, n = sc.pending_rows;
     err_any |= *(volatile int32_t*)(P + err_off);
@@ -780,7 +849,8 @@ tbn_status tbn_sparsemax_host_f64(const double* z, int64_t rows, int32_t n, doub
   if (tbn_device_count() <= 0) return fail(TBN_ERR_CUDA, "no CUDA device available");
   int dev = 0;
   cudaGetDevice(&dev);
-  HostCtx* hc = host_ctx(dev);
+  CtxLease lease(dev);
+  HostCtx* hc = lease.hc;
   if (!hc) return fail(TBN_ERR_CUDA, "cannot create stream");
   StreamCtx* c = &hc->s[0];
   // float64 end to end (the reference helper's precision, any width)

@@ -169,7 +169,7 @@ def test_load_invariance_bitwise(precision):
 @pytest.mark.parametrize("precision", ["bf16", "tf32x3"])
 def test_load_invariance_bitwise_wide(precision):
     """K3 / K3X (one tile per CTA, streamed weights, per-CTA scratch in the
-    per-thread host context's workspace): batch size 1 vs 96 and 1 vs 16
+    leased host context's workspace): batch size 1 vs 96 and 1 vs 16
     concurrent callers, bitwise."""
     m = P.TabNetModel.from_reference(W.make_model("wide"), precision=precision)
     x = W.make_inputs(W.WORKLOADS["wide"], 96).astype(np.float64)
@@ -179,7 +179,7 @@ def test_load_invariance_bitwise_wide(precision):
 def test_mixed_models_concurrent_threads():
     """Several models and kernels (K2 bf16 / 3xTF32, K3, K3X, the fp32 kernel)
     served from 12 threads at once on one device: every result equals the
-    same call made alone (per-thread host contexts, per-model workspaces)."""
+    same call made alone (leased host contexts, per-model workspaces)."""
     from concurrent.futures import ThreadPoolExecutor
     cases = [("hr", "bf16"), ("hr", "tf32x3"), ("wide", "bf16"), ("wide", "tf32x3"), ("adult", "fp32"),
              ("bls", "bf16")]

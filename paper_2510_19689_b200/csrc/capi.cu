@@ -526,12 +526,18 @@ struct DrainOnError {
   }
 };
 
-// Staging grows to the next power of two (at least 1 MB): each reallocation
-// (cudaFreeHost / cudaFree synchronise with the whole device) happens at most
-// log2 times per context.
+// Staging grows in steps of 4x from 8 MB (HR: ~7,000 rows) to 128 MB, then in
+// 128 MB steps: page-locking
+// costs ~2-4 ms per call to cudaMallocHost alone (tools/pin_cost.py) and
+// 50-180 ms when it contends with other threads' work inside a serving
+// process, so it should happen about once per context.  Requests of a few
+// bytes (the error-flag slot of the direct path) stay small.
 size_t staging_size(size_t need) {
-  size_t v = (size_t)1 << 20;
-  while (v < need) v <<= 1;
+  if (need <= 4096) return 4096;
+  const size_t big = (size_t)128 << 20;        // above: the next multiple of 128 MB (no 4x overshoot)
+  if (need > big) return (need + big - 1) / big * big;
+  size_t v = (size_t)8 << 20;
+  while (v < need) v <<= 2;
   return v;
 }
 cudaError_t ensure(StreamCtx* c, size_t pin_bytes, size_t dev_bytes) {
@@ -672,10 +678,12 @@ tbn_status forward_host_impl(const tbn_model* m, const T* x, int64_t rows, uint3
   DrainOnError drain_guard{hc};
   {
     NvtxRange nv_ensure("tbn_host: staging allocation");
-    for (auto& sc : hc->s) {
+    const int64_t nchunks = (rows + chunk - 1) / chunk;      // streams this call uses
+    for (int i = 0; i < kNumStreams; ++i) {
+      StreamCtx& sc = hc->s[i];
       if (sc.pending_r0 >= 0) TBN_CUDA(cudaStreamSynchronize(sc.stream));   // (defensive: never left set)
       sc.pending_r0 = -1;
-      TBN_CUDA(ensure(&sc, direct ? 256 : L.total, L.total));
+      if (i < nchunks) TBN_CUDA(ensure(&sc, direct ? 256 : L.total, L.total));
     }
   }
   int32_t err_any = 0;

@@ -107,12 +107,16 @@ uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
 }
 
 const char* kHeaders[] = {"k2_kernel.cuh", "tc_kernel.cuh", "tc_ptx.cuh", "tbn_rtc.h", "tbn_args.h"};
-constexpr int kLayoutInts = 28;
+constexpr int kLayoutInts = 31;
 
+// The throughput instance (up to 4 row groups) and the latency instance (at
+// most 2) of one shape, as for the prebuilt shapes (kernel_k2.cu): same
+// weight image, same arithmetic.
 struct JitK2 {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t kern = nullptr;
+  cudaKernel_t kern = nullptr, kern_lat = nullptr;
   K2Layout L;
+  int smem_lat = 0, threads_lat = 0;
   std::mutex attr_mu;
   bool attr_set[kMaxDevices] = {};
 };
@@ -138,15 +142,15 @@ void mkdirs(const std::string& d) {
 }
 
 // NVRTC-compile the K2 instance + layout query for one shape; returns the cubin
-bool compile(const std::string& src, const std::string& kname, std::vector<char>* cubin, std::string* lowered,
-             std::string* log_out) {
+bool compile(const std::string& src, const std::vector<std::string>& knames, std::vector<char>* cubin,
+             std::vector<std::string>* lowered, std::string* log_out) {
   const Nvrtc& nv = nvrtc();
   void* prog = nullptr;
   if (nv.create(&prog, src.c_str(), "tbn_k2_jit.cu", 0, nullptr, nullptr) != 0) {
     *log_out = "nvrtcCreateProgram failed";
     return false;
   }
-  nv.add_name(prog, kname.c_str());
+  for (const std::string& k : knames) nv.add_name(prog, k.c_str());
   const std::string inc_csrc = "-I" + lib_dir() + "/csrc";
   const char* cuda_inc_env = std::getenv("TBN_CUDA_INC");
   const std::string inc_cuda = std::string("-I") + (cuda_inc_env ? cuda_inc_env : TBN_CUDA_INC);
@@ -164,9 +168,12 @@ bool compile(const std::string& src, const std::string& kname, std::vector<char>
     nv.cubin_size(prog, &n);
     cubin->resize(n);
     nv.cubin(prog, cubin->data());
-    const char* low = nullptr;
-    ok = nv.lowered(prog, kname.c_str(), &low) == 0 && low;
-    if (ok) *lowered = low;
+    lowered->clear();
+    for (const std::string& k : knames) {
+      const char* low = nullptr;
+      ok = ok && nv.lowered(prog, k.c_str(), &low) == 0 && low;
+      if (ok) lowered->push_back(low);
+    }
   }
   nv.destroy(&prog);
   return ok;
@@ -183,16 +190,23 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
   char shape[128];
   std::snprintf(shape, sizeof(shape), "%d, %d, %d, %d, %d, %d", hp.F, hp.ND, hp.NA, hp.S, hp.C, prec);
   const std::string cfg = std::string("tbn::k2::Cfg<") + shape + ">";
-  const std::string kname = "tbn::k2::tabnet_rowthread<" + cfg + ">";
+  const std::string cfl = std::string("tbn::k2::Cfg<") + shape + ", 2>";
+  const std::vector<std::string> knames = {"tbn::k2::tabnet_rowthread<" + cfg + ">",
+                                           "tbn::k2::tabnet_rowthread<" + cfl + ">"};
   std::ostringstream src;
   src << "#include \"k2_kernel.cuh\"\n"
       << "typedef " << cfg << " JCF;\n"
+      << "typedef " << cfl << " JCL;\n"
+      << "static_assert(JCF::IMG_BYTES == JCL::IMG_BYTES && JCF::O_ATT == JCL::O_ATT && JCF::O_FC2 == JCL::O_FC2 &&\n"
+      << "              JCF::C_HB == JCL::C_HB, \"the latency instance must read the same weight image\");\n"
       << "template __global__ void tbn::k2::tabnet_rowthread<JCF>(tbn::k2::Params, tbn::ForwardArgs);\n"
+      << "template __global__ void tbn::k2::tabnet_rowthread<JCL>(tbn::k2::Params, tbn::ForwardArgs);\n"
       << "extern \"C\" __global__ void tbn_k2_layout(int* o) {\n"
       << "  const int v[] = {JCF::F, JCF::ND, JCF::NA, JCF::S, JCF::C, JCF::X3, JCF::BF, JCF::H, JCF::N2, JCF::NP,\n"
       << "    JCF::K1, JCF::KHID, JCF::KATT, JCF::FN, JCF::C_SCALE, JCF::C_SHIFT, JCF::C_HW, JCF::C_HB,\n"
       << "    JCF::O_SH1, JCF::O_SH2, JCF::O_FC1, JCF::O_FC2, JCF::O_ATT, tbn::tc::rup(JCF::B_HID, 128),\n"
-      << "    tbn::tc::rup(JCF::B_ATT, 128), JCF::IMG_BYTES, JCF::SMEM_BYTES, JCF::THREADS};\n"
+      << "    tbn::tc::rup(JCF::B_ATT, 128), JCF::IMG_BYTES, JCF::SMEM_BYTES, JCF::THREADS,\n"
+      << "    JCL::SMEM_BYTES, JCL::THREADS, JCL::NG};\n"
       << "  for (int i = 0; i < " << kLayoutInts << "; ++i) o[i] = v[i];\n}\n";
   const std::string source = src.str();
   const std::string key = source + "|" + hdrs;
@@ -206,13 +220,14 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
   const std::string cdir = cache_dir();
   const std::string cpath = cdir + "/k2_" + hex + ".cubin", npath = cdir + "/k2_" + hex + ".name";
   std::vector<char> cubin;
-  std::string lowered;
+  std::vector<std::string> lowered;
   {
     const std::string c = read_file(cpath), nm = read_file(npath);
-    if (!c.empty() && !nm.empty()) {
-      cubin.assign(c.begin(), c.end());
-      lowered = nm;
-    }
+    std::istringstream names(nm);
+    for (std::string line; std::getline(names, line);)
+      if (!line.empty()) lowered.push_back(line);
+    if (!c.empty() && lowered.size() == knames.size()) cubin.assign(c.begin(), c.end());
+    else lowered.clear();
   }
   if (cubin.empty()) {
     if (!nvrtc().ok) {
@@ -220,17 +235,21 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
       return nullptr;
     }
     std::string log;
-    if (!compile(source, kname, &cubin, &lowered, &log)) {
+    if (!compile(source, knames, &cubin, &lowered, &log)) {
       *err = "unsupported: K2 does not compile for this shape: " + log.substr(0, 600);
       return nullptr;
     }
     mkdirs(cdir);
     std::ofstream(cpath, std::ios::binary).write(cubin.data(), (std::streamsize)cubin.size());
-    std::ofstream(npath, std::ios::binary) << lowered;
+    {
+      std::ofstream nf(npath, std::ios::binary);
+      for (const std::string& l : lowered) nf << l << "\n";
+    }
   }
   std::unique_ptr<JitK2> j(new JitK2());
   cudaError_t e = cudaLibraryLoadData(&j->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  if (e == cudaSuccess) e = cudaLibraryGetKernel(&j->kern, j->lib, lowered.c_str());
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&j->kern, j->lib, lowered[0].c_str());
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&j->kern_lat, j->lib, lowered[1].c_str());
   cudaKernel_t q = nullptr;
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&q, j->lib, "tbn_k2_layout");
   int* d = nullptr;
@@ -255,6 +274,9 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
   L.C_SCALE = h[i++]; L.C_SHIFT = h[i++]; L.C_HW = h[i++]; L.C_HB = h[i++];
   L.O_SH1 = h[i++]; L.O_SH2 = h[i++]; L.O_FC1 = h[i++]; L.O_FC2 = h[i++]; L.O_ATT = h[i++];
   L.HBR = h[i++]; L.ABR = h[i++]; L.IMG_BYTES = h[i++]; L.SMEM_BYTES = h[i++]; L.THREADS = h[i++];
+  j->smem_lat = h[i++];
+  j->threads_lat = h[i++];
+  i++;                                      // JCL::NG (= threads_lat / 128)
   JitK2* raw = j.get();
   g_cache[key] = std::move(j);
   return raw;
@@ -297,28 +319,45 @@ cudaError_t k2_jit_launch(const TcModel& m, const ForwardArgs& a, int num_sms, c
     std::lock_guard<std::mutex> lk(j->attr_mu);
     if (!j->attr_set[dev]) {
       e = cudaFuncSetAttribute((const void*)j->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, j->L.SMEM_BYTES);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)j->kern_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, j->smem_lat);
       if (e != cudaSuccess) return e;
       j->attr_set[dev] = true;
     }
   }
-  // the same geometry as the prebuilt instances (kernel_k2.cu launch_k2_impl)
-  const int64_t ng = j->L.THREADS / 128;
-  const int64_t nq = a.packed ? (a.rows + 128 * ng - 1) / (128 * ng) : (a.rows + 127) / 128;
-  const int grid = (int)(nq < num_sms ? nq : num_sms);
+  // the same geometry and instance choice as the prebuilt instances
+  // (kernel_k2.cu launch_k2_impl)
+  auto grid_for = [&](int64_t ng) {
+    const int64_t nq = a.packed ? (a.rows + 128 * ng - 1) / (128 * ng) : (a.rows + 127) / 128;
+    return (int)(nq < num_sms ? nq : num_sms);
+  };
+  const int64_t ng = j->L.THREADS / 128, ng_lat = j->threads_lat / 128;
+  const void* kern = (const void*)j->kern;
+  int threads = j->L.THREADS, smem = j->L.SMEM_BYTES, grid = grid_for(ng);
+  if (ng_lat < ng && !a.packed) {
+    const int gl = grid_for(ng_lat);
+    const int64_t rpc = (((a.rows + gl - 1) / gl) + 3) & ~(int64_t)3;
+    if ((rpc + 127) / 128 <= ng_lat) {
+      kern = (const void*)j->kern_lat;
+      threads = j->threads_lat;
+      smem = j->smem_lat;
+      grid = gl;
+    }
+  }
   k2::Params p = *(const k2::Params*)m.params;
   ForwardArgs fa = a;
   void* args[] = {&p, &fa};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(j->L.THREADS);
-  cfg.dynamicSmemBytes = j->L.SMEM_BYTES;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL, as the prebuilt K2
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelExC(&cfg, (const void*)j->kern, args);
+  return cudaLaunchKernelExC(&cfg, kern, args);
 }
 
 }  // namespace tbn

@@ -805,7 +805,9 @@ def end_to_end(torch, dev, model, w, sr, rank, world, dist, a) -> dict:
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": 1e3 * float(te.item()) / steps,
            "rows_per_step": rows,
-           "path": "tbn_forward_host (C-ABI, pinned host fp32 buffers, 3-stream chunked H2D/kernel/D2H)"}
+           "path": ("tbn_forward_host (C-ABI, pinned host fp32 buffers; " +
+                    ("one zero-copy kernel: x read and outputs written over PCIe by the kernel)" if rows <= 32768
+                     else "3-stream chunked H2D/kernel/D2H)"))}
     if rows <= 262144:
         # the reference's own call shape: TabNetModel.apply on float64 numpy in/out
         # (network.py:195-267), host conversions included

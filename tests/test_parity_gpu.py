@@ -819,3 +819,21 @@ def test_runtime_compiled_k2_shapes(shape, precision):
         assert np.array_equal(big.masks[:, k:k + 1500], r.masks), k
         assert np.array_equal(big.probabilities[k:k + 1500], r.probabilities), k
         assert np.array_equal(big.importance[k:k + 1500], r.importance), k
+
+
+def test_leased_host_contexts_short_lived_threads():
+    """Host contexts are leased per call from a per-device pool: many short-lived
+    thread pools (as InferenceService workers and invariance.py's per-check
+    32-thread pool create) calling concurrently with mixed batch sizes and both
+    host paths (zero-copy and chunked) return exactly the serial results."""
+    from concurrent.futures import ThreadPoolExecutor
+    m = P.TabNetModel.from_reference(W.make_model("hr"), precision="bf16")
+    sizes = (1, 7, 300, 4096, 20000, 40000)
+    xs = {n: W.make_inputs(W.WORKLOADS["hr"], n, seed=n).astype(np.float64) for n in sizes}
+    ref = {n: m.apply(xs[n]) for n in sizes}
+    for rnd in range(4):
+        with ThreadPoolExecutor(max_workers=8) as pool:
+            jobs = [sizes[(i + rnd) % len(sizes)] for i in range(24)]
+            outs = list(pool.map(lambda n: (n, m.apply(xs[n])), jobs))
+        for n, r in outs:
+            assert np.array_equal(r.masks, ref[n].masks) and np.array_equal(r.probabilities, ref[n].probabilities), n

@@ -4,7 +4,7 @@
 # instance so one finding does not hide the next; logs in gpurun_out/sanitizer/.
 mkdir -p gpurun_out/sanitizer
 : > gpurun_out/sanitizer/summary.txt
-CASES="adult/bf16 adult/tf32x3 hr/bf16 hr/tf32 hr/tf32x3 bls/bf16 bls/tf32x3 bls/tf32 wide/bf16 wide/tf32x3 hr/fp32 wide/fp32 aux"
+CASES="adult/bf16 adult/tf32x3 hr/bf16 hr/tf32 hr/tf32x3 bls/bf16 bls/tf32x3 bls/tf32 wide/bf16 wide/tf32x3 hr/fp32 wide/fp32 jit aux"
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ "$tool" = "racecheck" ] && extra="--racecheck-report all"

@@ -37,6 +37,23 @@ for name, prec in cases:
     del xp, op
     print("ok", name, prec, flush=True)
     del r, m
+if which in ("all", "jit"):
+    # a runtime-compiled (NVRTC) K2 shape: the paper's own model (F=35, n_d=n_a=8, S=3),
+    # its latency instance (300 rows) and throughput instance (packed, 1,200 rows)
+    cfg = P.ModelConfig(feature_count=35, n_classes=2, n_d=8, n_a=8, n_steps=3, seed=0)
+    rng = np.random.default_rng(3)
+    for prec in ("bf16", "tf32x3"):
+        mj = P.TabNetModel(config=cfg, params=P.init_parameters(cfg), norm_mean=rng.standard_normal(35),
+                           norm_var=rng.uniform(0.5, 2.0, 35), model_version="jit35", precision=prec)
+        from paper_2510_19689_b200 import _native as N
+        for rows, fl in ((300, 0), (1200, N.FLAG_PACKED)):
+            rj = DeviceRunner(mj, rows, device=0, flags=fl)
+            rj.run(torch.from_numpy(np.random.default_rng(rows).standard_normal((rows, 35)).astype(np.float32)).cuda())
+            torch.cuda.synchronize()
+            rj.check_finite()
+            del rj
+        del mj
+    print("ok jit", flush=True)
 if which in ("all", "aux"):
     print(P.sparsemax(np.random.default_rng(0).standard_normal((100, 35))).shape)
     print(P.sparsemax(np.random.default_rng(0).standard_normal((10, 700))).shape)   # float64 kernel

@@ -249,6 +249,15 @@ __device__ __forceinline__ void ld32h(const uint16_t* p, float (&v)[32], uint64_
   }
 }
 
+// The per-feature-chunk loops that read the row-state scratch: unrolled by
+// TBN_K3_UNR so the next chunk's L2 loads are in flight while this one is used.
+#ifndef TBN_K3_UNR
+#define TBN_K3_UNR 1
+#endif
+#define TBN_K3_STR2(x) #x
+#define TBN_K3_STR(x) TBN_K3_STR2(x)
+#define K3_SCRATCH_UNROLL _Pragma(TBN_K3_STR(unroll TBN_K3_UNR))
+
 template <class CF>
 __global__ void __launch_bounds__(CF::THREADS, 1)
 tabnet_wide(const Params p, const ForwardArgs a) {
@@ -566,7 +575,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
     auto agg_update = [&]() {
       if (!agg_pend) return;
       agg_pend = false;
-#pragma unroll 1
+K3_SCRATCH_UNROLL
       for (int o = 0; o < FS; o += 32) {
         float mv[32], ag[32];
         ld32h(my_msk + (o / 8) * 1024, mv, pol);
@@ -588,7 +597,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       if (threadIdx.x == 0) TBN_K3T(1000 + 10 * s, clock64());
       // z' = prior * z in TMEM; slice max / sum
       float pmax = -INFINITY, psum = 0.0f;
-#pragma unroll 1
+K3_SCRATCH_UNROLL
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
         if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr, pol);   // in flight with the TMEM load
@@ -656,7 +665,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       // the mask goes to the coalesced scratch (read back for x*m and the agg
       // update) and, when requested, to the masks output
       float* mrow = a.masks ? a.masks + ((int64_t)(s - 1) * a.rows + wrow0) * F + c * FS : nullptr;
-#pragma unroll 1
+K3_SCRATCH_UNROLL
       for (int o = 0; o < FS; o += 32) {
         float z[32], pr[32];
         if (s > 1) ld32h(my_prior + (o / 8) * 1024, pr, pol);
@@ -675,7 +684,7 @@ tabnet_wide(const Params p, const ForwardArgs a) {
       if (threadIdx.x == 0) TBN_K3T(1003 + 10 * s, clock64());
       ptx::named_bar_sync(qbar, 128);                // every slice of the quarter is done with z
       // x * mask -> shared1 A (network.py:238), bf16, slice c -> A cols [64c, 64c + 64)
-#pragma unroll 1
+K3_SCRATCH_UNROLL
       for (int o = 0; o < FS; o += 32) {
         float xv[32], mv[32];
         ld32h(my_msk + (o / 8) * 1024, mv, pol);

@@ -74,6 +74,8 @@ def parse(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-share", action="store_true",
+                    help="skip the north-star share sub-object (HR: 8,192-row batches, one GPU's share of 65,536 on 8)")
     ap.add_argument("--no-parity-mode", action="store_true",
                     help="skip the tf32x3 (parity mode) timing sub-object")
     ap.add_argument("--no-graph", action="store_true",
@@ -639,6 +641,12 @@ def run_ours(a) -> None:
     if not a.no_parity_mode and a.precision != "tf32x3" and use_graph:
         parity = parity_mode(torch, dev, w, a, rows, start, local, counts, world, dist)
 
+    # ---- the north star's per-GPU share (65,536 rows over 8 GPUs = 8,192 rows per GPU)
+    share = None
+    if (a.config == "hr" and rows == 65536 and world == 1 and not a.no_share and use_graph
+            and a.precision == "bf16"):
+        share = north_star_share(torch, dev, model, w, start, local, counts, world, dist)
+
     # ---- end to end through the C-ABI host call: pinned host in/out, H2D+D2H timed
     e2e = None
     if not a.no_e2e:
@@ -691,6 +699,7 @@ def run_ours(a) -> None:
                                                   + ("; max over ranks per step)" if world > 1 else ")")},
             "steady_state": steady,
             "parity_mode": parity,
+            "north_star_share": share,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": a.steps * launches_per_step,
@@ -747,6 +756,28 @@ def steady_state(torch, dev, model, w, rows, start, local, q, counts, world, dis
             "ms_per_round": ms / ks, "hbm_frac": frac,
             "how": f"{q} streams per GPU, each launching its own {rows}-row batch per round (TBN_FLAG_PACKED), "
                    f"{ks} rounds in one CUDA graph, max over ranks"}
+
+
+def north_star_share(torch, dev, model, w, start, local, counts, world, dist) -> dict:
+    """One GPU's share of the north star's HR batch (65,536 rows row-sharded
+    over 8 GPUs, no collective): 8,192-row batches back to back on one stream
+    (each a single tile chain per SM), and 16 such batches in flight."""
+    rows = 65536 // 8
+    sr = StepRunner(model, w, rows, start, local, flush_ok=False)
+    ks = 20
+    g = capture(torch, dev, lambda s: [sr.launch(s) for _ in range(ks)])
+    g.replay()
+    torch.cuda.synchronize()
+    ms = time_graph(torch, g, torch.cuda.current_stream(dev)) / ks
+    sr.runner.check_finite()
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = peaks.get("hbm_gbs", 6650.0) * 1e9
+    ss = steady_state(torch, dev, model, w, rows, start, local, 16, counts, world, dist)
+    return {"rows_per_gpu": rows, "gpus": 8,
+            "one_batch": {"us": ms * 1e3, "rows_per_s": rows / (ms / 1e3),
+                          "hbm_frac": counts["bytes_per_row"] * rows / (ms / 1e3) / hbm,
+                          "how": f"{ks} back-to-back 8,192-row batches on one stream in one CUDA graph"},
+            "inflight_16": {"rows_per_s": ss["value"], "hbm_frac": ss["hbm_frac"], "how": ss["how"]}}
 
 
 def parity_mode(torch, dev, w, a, rows, start, local, counts, world, dist) -> dict | None:

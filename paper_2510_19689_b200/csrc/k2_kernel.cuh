@@ -60,9 +60,18 @@ constexpr int pow2ceil(int v) { int p = 32; while (p < v) p <<= 1; return p; }
 // (kernel_k2.cu), used when a CTA gets at most 2 row tiles: more registers per
 // thread, xn in registers and (for HR) resident weights shorten the tile chain.
 // The arithmetic is the same in both, so outputs are bitwise identical.
-template <int F_, int ND_, int NA_, int S_, int C_, int PREC_, int MAXNG_ = TBN_K2_MAXNG>
+// SPLIT_ (with MAXNG_ = 1): the split latency instance, used when a CTA gets a
+// single row tile.  One row group of 8 warps: warp q (the row's owner) does
+// everything K2 does but compute only the d-half GLU columns [0, n_d); warp
+// q + 4 (its helper, same TMEM lanes, same SMSP) computes the a-half [n_d, h)
+// and writes the attentive A.  The two halves of a GLU layer run side by side
+// instead of one after the other (a tile chain is latency-bound: one warp per
+// SMSP); per-column arithmetic is unchanged, so outputs stay bitwise identical.
+template <int F_, int ND_, int NA_, int S_, int C_, int PREC_, int MAXNG_ = TBN_K2_MAXNG, bool SPLIT_ = false>
 struct Cfg {
   static constexpr int F = F_, ND = ND_, NA = NA_, S = S_, C = C_, PREC = PREC_;
+  static constexpr bool SPLIT = SPLIT_;
+  static_assert(!SPLIT || (MAXNG_ == 1 && ND % 2 == 0 && NA % 2 == 0), "split instance: one group, even halves");
   static_assert(PREC == kPrecTF32 || PREC == kPrecBF16 || PREC == tc::kPrecTF32x3, "K2 precision");
   static constexpr int H = ND + NA, N2 = 2 * H;
   // MMA N of the GLU GEMMs: 2h padded to the M=128 granule (B rows beyond 2h are 0)
@@ -130,8 +139,10 @@ struct Cfg {
   static constexpr int TCOLS = pow2ceil(NG * TCG);
   static_assert(TCOLS <= 512, "TMEM");
   static_assert(NP <= 256 && FN <= 256, "MMA N > 256");
-  static constexpr int THREADS = NG * 128;
-  static constexpr int NW = NG * 4;
+  static_assert(!SPLIT || !RING, "split instance: weights resident");
+  static constexpr int THREADS = NG * 128 * (SPLIT ? 2 : 1);
+  static constexpr int NW = NG * 4 * (SPLIT ? 2 : 1);
+  static constexpr int BAR_THREADS = SPLIT ? 256 : 128;   // one group's named barrier
   // shared-memory plan: resident image (or its fixed part + att + ring) | staging | bars
   static constexpr int S_ATT = RING ? O_FC1 : O_ATT;   // where att_1 lives in SMEM
   static constexpr int OFF_RING = O_FC1 + S * ABR;
@@ -238,7 +249,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   // warp index through a shuffle: provably warp-uniform, so the TMEM and SMEM
   // addresses derived from it live in uniform registers (no R2UR per tcgen05 op)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int g = warp >> 2, q = warp & 3;
+  const bool helper = CF::SPLIT && warp >= 4;      // split instance: the a-half warp
+  const int g = CF::SPLIT ? 0 : warp >> 2, q = warp & 3;
   const int t = q * 32 + lane;                      // row within the tile == TMEM lane
   const bool x_bulk_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15u) == 0);
   // this CTA's rows: a contiguous block of R = ceil(rows / grid) rounded up to 4
@@ -375,7 +387,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       // kernel's writes land, so a prefetch ahead of the wait cannot read stale data)
     int64_t r0p;
     const int nwp = warp_rows(g, r0p);
-    if (lane == 0 && nwp > 0 && x_bulk_ok) {
+    if (lane == 0 && nwp > 0 && x_bulk_ok && !helper) {
       const uint32_t bytes = (uint32_t)((nwp * F * 4) & ~15);
       if (bytes) ptx::bulk_prefetch_l2(a.x + r0p * F, bytes);
     }
@@ -387,7 +399,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   {   // this warp's first x tile
     int64_t r0w;
     const int nw0 = warp_rows(g, r0w);
-    if (nw0 > 0) issue_x(r0w, nw0);
+    if (nw0 > 0 && !helper) issue_x(r0w, nw0);
   }
   ptx::mbar_wait(&bars->cfull, 0);                   // the weights have landed
   if (a.scale) {     // batch-statistics control: override the affine in this CTA's copy
@@ -405,7 +417,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
   // chain and commits it; `post` overlaps the MMA; then everyone waits for D.
   int jt = 0;                                    // trace: GEMM counter
   int64_t ring_pending = -1;                     // ring block awaiting release (same in every warp)
-  const bool tr = (q == 0 && lane == 0);
+  const bool tr = (q == 0 && lane == 0 && !helper);
   auto gemm = [&](int kind, uint32_t bo, int64_t rv, auto&& post) {
     if (tr) TBN_TRACE(g * 4000 + 4 * jt);
     // the issuing warp rotates over the group's four warps (measured 1.3%
@@ -416,7 +428,7 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       // writing A (off the barrier -> MMA critical path)
       if (rv >= 0) {
         const uint32_t v = (uint32_t)rv;
-        if (q == iq) ptx::mbar_wait(&bars->rfull[ring_slot(v)], ring_parity(v));
+        if (q == iq && !helper) ptx::mbar_wait(&bars->rfull[ring_slot(v)], ring_parity(v));
         bo = CF::OFF_RING + ring_slot(v) * CF::HBR;
       }
     }
@@ -424,10 +436,10 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
 #ifndef TBN_K2_NOBAR          // dev experiment only (with TBN_K2_NOMMA): the barrier's cost
-    ptx::named_bar_sync(bar_id, 128);
+    ptx::named_bar_sync(bar_id, CF::BAR_THREADS);
 #endif
     if (tr) TBN_TRACE(g * 4000 + 4 * jt + 1);
-    if (q == iq) {
+    if (q == iq && !helper) {
       ptx::tc_fence_after();
       const uint32_t tAL = tA + CF::KA;              // A_lo (3xTF32 only)
 #ifndef TBN_K2_NOMMA          // dev experiment only: the tensor core's share of the chain
@@ -520,8 +532,10 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       }
     }
   };
-  auto glu = [&](bool residual) { glu_range(residual, std::integral_constant<int, 0>{}, std::integral_constant<int, H>{}); };
-  auto store_g = [&]() { put_a<CF, CF::A0, H>(tA, gv); };
+  // the owner's GLU columns: all h, or the d-half [0, n_d) in the split instance
+  constexpr int GE = CF::SPLIT ? ND : H;
+  auto glu = [&](bool residual) { glu_range(residual, std::integral_constant<int, 0>{}, std::integral_constant<int, GE>{}); };
+  auto store_g = [&]() { put_a<CF, CF::A0, GE>(tA, gv); };
 
 #ifdef TBN_K2_STAGGER      // dev experiment: de-phase the groups' chains
   {
@@ -576,6 +590,42 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
         skel(s);
       }
       continue;
+    }
+    if constexpr (CF::SPLIT) {
+      if (helper) {
+        // split instance, warp q + 4: the a-half [n_d, h) of every GLU layer and
+        // the attentive A (a = f[:, n_d:], network.py:233), same GEMM sequence
+        auto hglu = [&](bool residual) {
+          glu_range(residual, std::integral_constant<int, ND>{}, std::integral_constant<int, H>{});
+        };
+        auto hstore = [&](auto e0) {
+          float av[NA];
+#pragma unroll
+          for (int e = 0; e < NA; ++e) av[e] = gv[ND + e];
+          put_a<CF, decltype(e0)::value, NA>(tA, av);
+        };
+        auto htransform = [&](int s) {
+          const std::integral_constant<int, CF::A0 + ND> at_a;
+          gemm(0, CF::O_SH1, -1, nopost);
+          hglu(false);
+          hstore(at_a);
+          gemm(1, CF::O_SH2, -1, nopost);
+          hglu(true);
+          hstore(at_a);
+          gemm(1, CF::O_FC1 + (uint32_t)s * CF::HBR, -1, nopost);
+          hglu(true);
+          hstore(at_a);
+          gemm(1, CF::O_FC2 + (uint32_t)s * CF::HBR, -1, nopost);
+          if (s != S) hglu(true);          // step S's a-half is unused
+        };
+        htransform(0);
+        for (int s = 1; s <= S; ++s) {
+          hstore(std::integral_constant<int, CF::A0>{});
+          gemm(2, CF::S_ATT + (uint32_t)(s - 1) * CF::ABR, -1, nopost);
+          htransform(s);
+        }
+        continue;
+      }
     }
 
     // ---- x -> xn (network.py:118-120), prior = 1, agg = 0 ----
@@ -653,7 +703,8 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
       store_g();
       gemm(1, o2, CF::RING ? rv0 + 2 * s + 1 : -1, nopost);
 #ifndef TBN_K2_NOPRUNE     // the unused halves are skipped: +0.7%
-      if constexpr (ND % 2 != 0) glu(true);     // (pairs would straddle the d/a boundary)
+      if constexpr (CF::SPLIT) { if (s != 0) glu(true); }    // (the helper: the a-half)
+      else if constexpr (ND % 2 != 0) glu(true);     // (pairs would straddle the d/a boundary)
       else if (s == 0) glu_range(true, std::integral_constant<int, ND>{}, std::integral_constant<int, H>{});
       else if (s == S) glu_range(true, std::integral_constant<int, 0>{}, std::integral_constant<int, ND>{});
       else glu(true);
@@ -705,7 +756,9 @@ tabnet_rowthread(const Params p, const ForwardArgs a) {
     for (int s = 1; s <= S; ++s) {
       // A <- [1, 1, a = f[:, n_d:]]; under the attentive MMA: the previous
       // step's d/eta/logits and agg update
-      {
+      if constexpr (CF::SPLIT) {
+        if (s > 1) eta_prev = step_eta();         // (the helper writes the attentive A)
+      } else {
         float av[NA];
 #pragma unroll
         for (int e = 0; e < NA; ++e) av[e] = gv[ND + e];

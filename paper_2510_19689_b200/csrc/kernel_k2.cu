@@ -6,6 +6,7 @@
 //   sigma(u) = (1 + tanh(u/2)) / 2   =>  gate columns x 1/2,
 //   linear columns x 1/2 (shared1) or x sqrt(1/2)/2 (the residual blocks
 //   shared2/fc1/fc2, network.py:131-137: (lin sigma + prev) sqrt(.5)).
+#include <type_traits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -123,18 +124,34 @@ cudaError_t launch_k2_cfg(const TcModel& m, const ForwardArgs& a, int grid, cuda
   return cudaLaunchKernelEx(&cfg, k2::tabnet_rowthread<CF>, *(const k2::Params*)m.params, a);
 }
 
+// The split latency instance of a shape (k2_kernel.cuh, Cfg::SPLIT) where its
+// one 8-warp group fits with every weight block resident; else none (the
+// 2-group latency instance stands in).
+template <int F, int ND, int NA, int S, int C, int P>
+struct SplitOf {
+  static constexpr bool ok = !k2::Cfg<F, ND, NA, S, C, P, 1>::RING && ND % 2 == 0 && NA % 2 == 0;
+  using type = std::conditional_t<ok, k2::Cfg<F, ND, NA, S, C, P, 1, true>, k2::Cfg<F, ND, NA, S, C, P, 2>>;
+};
+
 // CF: the throughput instance; CL: the latency instance of the same shape
-// (at most 2 row groups), launched when no CTA gets more than CL::NG tiles.
-// Both read the same weight image.
-template <class CF, class CL>
+// (at most 2 row groups), launched when no CTA gets more than CL::NG tiles;
+// CS: the split latency instance, launched when every CTA gets one tile.
+// All read the same weight image and give bitwise identical rows.
+template <class CF, class CL, class CS>
 cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, cudaStream_t stream) {
   static_assert(CF::IMG_BYTES == CL::IMG_BYTES && CF::O_ATT == CL::O_ATT && CF::O_FC2 == CL::O_FC2 &&
                 CF::C_HB == CL::C_HB, "the latency instance must read the same weight image");
+  static_assert(CF::IMG_BYTES == CS::IMG_BYTES && CF::O_ATT == CS::O_ATT && CF::O_FC2 == CS::O_FC2 &&
+                CF::C_HB == CS::C_HB, "the split instance must read the same weight image");
   if constexpr (CL::NG < CF::NG) {
     static const bool off = std::getenv("TBN_K2_NO_LATENCY") != nullptr;   // development A/B only
+    static const bool nosplit = std::getenv("TBN_K2_NO_SPLIT") != nullptr;  // development A/B only
     if (!a.packed && !off) {
       const int grid = k2_grid(a, num_sms, CL::NG);
       const int64_t rpc = (((a.rows + grid - 1) / grid) + 3) & ~(int64_t)3;
+      if constexpr (CS::SPLIT) {
+        if (rpc <= 128 && !nosplit) return launch_k2_cfg<CS>(m, a, grid, stream);
+      }
       if ((rpc + 127) / 128 <= CL::NG) return launch_k2_cfg<CL>(m, a, grid, stream);
     }
   }
@@ -143,7 +160,8 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
 
 #define TBN_K2(F, ND, NA, S, C, P)                                                  \
   K2Instance{F, ND, NA, S, C, P, &pack_k2<k2::Cfg<F, ND, NA, S, C, P>>,            \
-             &launch_k2_impl<k2::Cfg<F, ND, NA, S, C, P>, k2::Cfg<F, ND, NA, S, C, P, 2>>}
+             &launch_k2_impl<k2::Cfg<F, ND, NA, S, C, P>, k2::Cfg<F, ND, NA, S, C, P, 2>, \
+                             typename SplitOf<F, ND, NA, S, C, P>::type>}
 
 #ifdef TBN_K2_SINGLE   // dev A/B builds: one instance only, e.g. -DTBN_K2_SINGLE=K2_HR_BF16
 #define K2_HR_BF16 35, 16, 16, 5, 2, tc::kPrecBF16

@@ -616,9 +616,10 @@ def test_row_partition_geometry_bitwise(name, precision):
     contiguous row blocks per CTA, partial last tiles, warps without rows):
     the outputs of each row must not depend on it.  Odd sizes around the tile,
     warp and per-CTA boundaries, on the device path, against 1,000-row calls.
-    The 1,000-row calls and batches up to 2 tiles per CTA run K2's latency
-    instance (2 row groups), larger and packed batches the throughput instance
-    (up to 4): the two must agree bit for bit."""
+    The 1,000-row calls and batches of one tile per CTA run K2's split latency
+    instance (one 8-warp group, the GLU halves on two warps) where the shape has
+    one, batches up to 2 tiles per CTA the 2-group latency instance, larger and
+    packed batches the throughput instance (up to 4): all must agree bit for bit."""
     import torch
     from paper_2510_19689_b200.device import DeviceRunner
     m = P.TabNetModel.from_reference(W.make_model(name), precision=precision)
@@ -633,7 +634,7 @@ def test_row_partition_geometry_bitwise(name, precision):
     ref = {k: torch.cat(v, dim=1 if k == "masks" else 0) for k, v in ref.items()}
     from paper_2510_19689_b200 import _native as N
     packed = DeviceRunner(m, max_rows=big, flags=N.FLAG_PACKED)   # full tiles on fewer SMs
-    for rows in (1, 3, 31, 33, 127, 129, 443, 445, 4097, 8192, big):
+    for rows in (1, 3, 31, 33, 127, 129, 443, 445, 4097, 8192, 18944, 30001, big):
         for rn in (runner, packed):
             o = rn.run(x[:rows].contiguous())
             torch.cuda.synchronize()

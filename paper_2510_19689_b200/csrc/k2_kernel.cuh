@@ -139,7 +139,6 @@ struct Cfg {
   static constexpr int TCOLS = pow2ceil(NG * TCG);
   static_assert(TCOLS <= 512, "TMEM");
   static_assert(NP <= 256 && FN <= 256, "MMA N > 256");
-  static_assert(!SPLIT || !RING, "split instance: weights resident");
   static constexpr int THREADS = NG * 128 * (SPLIT ? 2 : 1);
   static constexpr int NW = NG * 4 * (SPLIT ? 2 : 1);
   static constexpr int BAR_THREADS = SPLIT ? 256 : 128;   // one group's named barrier

@@ -129,7 +129,8 @@ cudaError_t launch_k2_cfg(const TcModel& m, const ForwardArgs& a, int grid, cuda
 // 2-group latency instance stands in).
 template <int F, int ND, int NA, int S, int C, int P>
 struct SplitOf {
-  static constexpr bool ok = !k2::Cfg<F, ND, NA, S, C, P, 1>::RING && ND % 2 == 0 && NA % 2 == 0;
+  static constexpr bool ok = ND % 2 == 0 && NA % 2 == 0 &&
+                             (!k2::Cfg<F, ND, NA, S, C, P, 1>::RING || P == tc::kPrecTF32x3);
   using type = std::conditional_t<ok, k2::Cfg<F, ND, NA, S, C, P, 1, true>, k2::Cfg<F, ND, NA, S, C, P, 2>>;
 };
 
@@ -143,7 +144,7 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
                 CF::C_HB == CL::C_HB, "the latency instance must read the same weight image");
   static_assert(CF::IMG_BYTES == CS::IMG_BYTES && CF::O_ATT == CS::O_ATT && CF::O_FC2 == CS::O_FC2 &&
                 CF::C_HB == CS::C_HB, "the split instance must read the same weight image");
-  if constexpr (CL::NG < CF::NG) {
+  if constexpr (CS::SPLIT || CL::NG < CF::NG) {
     static const bool off = std::getenv("TBN_K2_NO_LATENCY") != nullptr;   // development A/B only
     static const bool nosplit = std::getenv("TBN_K2_NO_SPLIT") != nullptr;  // development A/B only
     if (!a.packed && !off) {
@@ -152,7 +153,9 @@ cudaError_t launch_k2_impl(const TcModel& m, const ForwardArgs& a, int num_sms, 
       if constexpr (CS::SPLIT) {
         if (rpc <= 128 && !nosplit) return launch_k2_cfg<CS>(m, a, grid, stream);
       }
-      if ((rpc + 127) / 128 <= CL::NG) return launch_k2_cfg<CL>(m, a, grid, stream);
+      if constexpr (CL::NG < CF::NG) {
+        if ((rpc + 127) / 128 <= CL::NG) return launch_k2_cfg<CL>(m, a, grid, stream);
+      }
     }
   }
   return launch_k2_cfg<CF>(m, a, k2_grid(a, num_sms, CF::NG), stream);

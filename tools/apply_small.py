@@ -2,7 +2,7 @@ import sys, time, json
 import numpy as np
 sys.path.insert(0, ".")
 from paper_2510_19689_b200 import workloads as W
-m = W.make_engine_model("hr", "trained", precision="bf16", device=0)
+m = W.make_engine_model("hr", "trained", precision=sys.argv[1] if len(sys.argv) > 1 else "bf16", device=0)
 res = {}
 for rows in (1, 16, 128, 512, 2048, 8192, 32768):
     x = W.make_inputs(W.WORKLOADS["hr"], rows).astype(np.float64)

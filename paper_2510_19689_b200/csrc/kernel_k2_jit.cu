@@ -107,16 +107,17 @@ uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
 }
 
 const char* kHeaders[] = {"k2_kernel.cuh", "tc_kernel.cuh", "tc_ptx.cuh", "tbn_rtc.h", "tbn_args.h"};
-constexpr int kLayoutInts = 31;
+constexpr int kLayoutInts = 33;
 
-// The throughput instance (up to 4 row groups) and the latency instance (at
-// most 2) of one shape, as for the prebuilt shapes (kernel_k2.cu): same
+// The throughput instance (up to 4 row groups), the latency instance (at
+// most 2) and, for even n_d and n_a, the split latency instance (one 8-warp
+// group) of one shape, as for the prebuilt shapes (kernel_k2.cu): same
 // weight image, same arithmetic.
 struct JitK2 {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t kern = nullptr, kern_lat = nullptr;
+  cudaKernel_t kern = nullptr, kern_lat = nullptr, kern_split = nullptr;
   K2Layout L;
-  int smem_lat = 0, threads_lat = 0;
+  int smem_lat = 0, threads_lat = 0, smem_split = 0, threads_split = 0;
   std::mutex attr_mu;
   bool attr_set[kMaxDevices] = {};
 };
@@ -191,36 +192,69 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
   std::snprintf(shape, sizeof(shape), "%d, %d, %d, %d, %d, %d", hp.F, hp.ND, hp.NA, hp.S, hp.C, prec);
   const std::string cfg = std::string("tbn::k2::Cfg<") + shape + ">";
   const std::string cfl = std::string("tbn::k2::Cfg<") + shape + ", 2>";
-  const std::vector<std::string> knames = {"tbn::k2::tabnet_rowthread<" + cfg + ">",
-                                           "tbn::k2::tabnet_rowthread<" + cfl + ">"};
-  std::ostringstream src;
-  src << "#include \"k2_kernel.cuh\"\n"
-      << "typedef " << cfg << " JCF;\n"
-      << "typedef " << cfl << " JCL;\n"
-      << "static_assert(JCF::IMG_BYTES == JCL::IMG_BYTES && JCF::O_ATT == JCL::O_ATT && JCF::O_FC2 == JCL::O_FC2 &&\n"
-      << "              JCF::C_HB == JCL::C_HB, \"the latency instance must read the same weight image\");\n"
-      << "template __global__ void tbn::k2::tabnet_rowthread<JCF>(tbn::k2::Params, tbn::ForwardArgs);\n"
-      << "template __global__ void tbn::k2::tabnet_rowthread<JCL>(tbn::k2::Params, tbn::ForwardArgs);\n"
-      << "extern \"C\" __global__ void tbn_k2_layout(int* o) {\n"
-      << "  const int v[] = {JCF::F, JCF::ND, JCF::NA, JCF::S, JCF::C, JCF::X3, JCF::BF, JCF::H, JCF::N2, JCF::NP,\n"
-      << "    JCF::K1, JCF::KHID, JCF::KATT, JCF::FN, JCF::C_SCALE, JCF::C_SHIFT, JCF::C_HW, JCF::C_HB,\n"
-      << "    JCF::O_SH1, JCF::O_SH2, JCF::O_FC1, JCF::O_FC2, JCF::O_ATT, tbn::tc::rup(JCF::B_HID, 128),\n"
-      << "    tbn::tc::rup(JCF::B_ATT, 128), JCF::IMG_BYTES, JCF::SMEM_BYTES, JCF::THREADS,\n"
-      << "    JCL::SMEM_BYTES, JCL::THREADS, JCL::NG};\n"
-      << "  for (int i = 0; i < " << kLayoutInts << "; ++i) o[i] = v[i];\n}\n";
-  const std::string source = src.str();
-  const std::string key = source + "|" + hdrs;
+  const std::string cfs = std::string("tbn::k2::Cfg<") + shape + ", 1, true>";
+  // the split instance where its halves are even; dropped again if it does not
+  // compile for the shape (e.g. no room for its staging next to a weight ring)
+  bool split = hp.ND % 2 == 0 && hp.NA % 2 == 0;
+  std::vector<std::string> knames;
+  std::string source, key;
+  auto make_source = [&]() {
+    knames = {"tbn::k2::tabnet_rowthread<" + cfg + ">", "tbn::k2::tabnet_rowthread<" + cfl + ">"};
+    if (split) knames.push_back("tbn::k2::tabnet_rowthread<" + cfs + ">");
+    std::ostringstream src;
+    src << "#include \"k2_kernel.cuh\"\n"
+        << "typedef " << cfg << " JCF;\n"
+        << "typedef " << cfl << " JCL;\n"
+        << "static_assert(JCF::IMG_BYTES == JCL::IMG_BYTES && JCF::O_ATT == JCL::O_ATT && JCF::O_FC2 == JCL::O_FC2 &&\n"
+        << "              JCF::C_HB == JCL::C_HB, \"the latency instance must read the same weight image\");\n"
+        << "template __global__ void tbn::k2::tabnet_rowthread<JCF>(tbn::k2::Params, tbn::ForwardArgs);\n"
+        << "template __global__ void tbn::k2::tabnet_rowthread<JCL>(tbn::k2::Params, tbn::ForwardArgs);\n";
+    if (split)
+      src << "typedef " << cfs << " JCS;\n"
+          << "static_assert(JCF::IMG_BYTES == JCS::IMG_BYTES && JCF::O_ATT == JCS::O_ATT && JCF::O_FC2 == JCS::O_FC2 &&\n"
+          << "              JCF::C_HB == JCS::C_HB, \"the split instance must read the same weight image\");\n"
+          << "template __global__ void tbn::k2::tabnet_rowthread<JCS>(tbn::k2::Params, tbn::ForwardArgs);\n";
+    src << "extern \"C\" __global__ void tbn_k2_layout(int* o) {\n"
+        << "  const int v[] = {JCF::F, JCF::ND, JCF::NA, JCF::S, JCF::C, JCF::X3, JCF::BF, JCF::H, JCF::N2, JCF::NP,\n"
+        << "    JCF::K1, JCF::KHID, JCF::KATT, JCF::FN, JCF::C_SCALE, JCF::C_SHIFT, JCF::C_HW, JCF::C_HB,\n"
+        << "    JCF::O_SH1, JCF::O_SH2, JCF::O_FC1, JCF::O_FC2, JCF::O_ATT, tbn::tc::rup(JCF::B_HID, 128),\n"
+        << "    tbn::tc::rup(JCF::B_ATT, 128), JCF::IMG_BYTES, JCF::SMEM_BYTES, JCF::THREADS,\n"
+        << "    JCL::SMEM_BYTES, JCL::THREADS, JCL::NG, "
+        << (split ? "JCS::SMEM_BYTES, JCS::THREADS" : "0, 0") << "};\n"
+        << "  for (int i = 0; i < " << kLayoutInts << "; ++i) o[i] = v[i];\n}\n";
+    source = src.str();
+    key = source + "|" + hdrs;
+  };
+  make_source();
 
   std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_cache.find(key);
-  if (it != g_cache.end()) return it->second.get();
+  {
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) return it->second.get();
+  }
 
-  char hex[32];
-  std::snprintf(hex, sizeof(hex), "%016llx", (unsigned long long)fnv1a(key));
   const std::string cdir = cache_dir();
-  const std::string cpath = cdir + "/k2_" + hex + ".cubin", npath = cdir + "/k2_" + hex + ".name";
+  std::string cpath, npath;
+  auto set_paths = [&]() {
+    char hex[32];
+    std::snprintf(hex, sizeof(hex), "%016llx", (unsigned long long)fnv1a(key));
+    cpath = cdir + "/k2_" + hex + ".cubin";
+    npath = cdir + "/k2_" + hex + ".name";
+  };
+  set_paths();
   std::vector<char> cubin;
   std::vector<std::string> lowered;
+  if (split && read_file(cpath).empty()) {
+    // a shape whose split instance failed to compile before is cached without it
+    split = false;
+    make_source();
+    set_paths();
+    if (read_file(cpath).empty()) {
+      split = true;
+      make_source();
+      set_paths();
+    }
+  }
   {
     const std::string c = read_file(cpath), nm = read_file(npath);
     std::istringstream names(nm);
@@ -235,7 +269,14 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
       return nullptr;
     }
     std::string log;
-    if (!compile(source, knames, &cubin, &lowered, &log)) {
+    bool ok = compile(source, knames, &cubin, &lowered, &log);
+    if (!ok && split) {                     // retry without the split instance
+      split = false;
+      make_source();
+      set_paths();
+      ok = compile(source, knames, &cubin, &lowered, &log);
+    }
+    if (!ok) {
       *err = "unsupported: K2 does not compile for this shape: " + log.substr(0, 600);
       return nullptr;
     }
@@ -250,6 +291,7 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
   cudaError_t e = cudaLibraryLoadData(&j->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&j->kern, j->lib, lowered[0].c_str());
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&j->kern_lat, j->lib, lowered[1].c_str());
+  if (e == cudaSuccess && split) e = cudaLibraryGetKernel(&j->kern_split, j->lib, lowered[2].c_str());
   cudaKernel_t q = nullptr;
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&q, j->lib, "tbn_k2_layout");
   int* d = nullptr;
@@ -277,6 +319,8 @@ JitK2* get_or_build(const HostParams& hp, int prec, std::string* err) {
   j->smem_lat = h[i++];
   j->threads_lat = h[i++];
   i++;                                      // JCL::NG (= threads_lat / 128)
+  j->smem_split = h[i++];
+  j->threads_split = h[i++];
   JitK2* raw = j.get();
   g_cache[key] = std::move(j);
   return raw;
@@ -321,6 +365,9 @@ cudaError_t k2_jit_launch(const TcModel& m, const ForwardArgs& a, int num_sms, c
       e = cudaFuncSetAttribute((const void*)j->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, j->L.SMEM_BYTES);
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute((const void*)j->kern_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, j->smem_lat);
+      if (e == cudaSuccess && j->kern_split)
+        e = cudaFuncSetAttribute((const void*)j->kern_split, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 j->smem_split);
       if (e != cudaSuccess) return e;
       j->attr_set[dev] = true;
     }
@@ -334,10 +381,16 @@ cudaError_t k2_jit_launch(const TcModel& m, const ForwardArgs& a, int num_sms, c
   const int64_t ng = j->L.THREADS / 128, ng_lat = j->threads_lat / 128;
   const void* kern = (const void*)j->kern;
   int threads = j->L.THREADS, smem = j->L.SMEM_BYTES, grid = grid_for(ng);
-  if (ng_lat < ng && !a.packed) {
+  static const bool nosplit = std::getenv("TBN_K2_NO_SPLIT") != nullptr;   // development A/B only
+  if ((ng_lat < ng || j->kern_split) && !a.packed) {
     const int gl = grid_for(ng_lat);
     const int64_t rpc = (((a.rows + gl - 1) / gl) + 3) & ~(int64_t)3;
-    if ((rpc + 127) / 128 <= ng_lat) {
+    if (j->kern_split && rpc <= 128 && !nosplit) {
+      kern = (const void*)j->kern_split;
+      threads = j->threads_split;
+      smem = j->smem_split;
+      grid = gl;
+    } else if (ng_lat < ng && (rpc + 127) / 128 <= ng_lat) {
       kern = (const void*)j->kern_lat;
       threads = j->threads_lat;
       smem = j->smem_lat;

@@ -812,9 +812,14 @@ def test_runtime_compiled_k2_shapes(shape, precision):
         mmax, mp999, imax, pmax = EMU_BOUNDS[precision]
         assert st["mask_max"] < mmax and st["mask_p999"] < mp999 and st["imp_max"] < imax and st["prob_max"] < pmax
     # batch invariance holds for the compiled-at-run-time kernel as well; the
-    # small calls run its latency instance, a 60,000-row call the throughput one
+    # small calls run its split latency instance, a 30,000-row call the 2-group
+    # latency instance, a 60,000-row call the throughput one
     part = m.apply(x[:333].astype(np.float64))
     assert np.array_equal(part.masks, r.masks[:, :333]) and np.array_equal(part.probabilities, r.probabilities[:333])
+    mid = m.apply(np.tile(x, (20, 1)).astype(np.float64))
+    for k in range(0, 30000, 7500):
+        assert np.array_equal(mid.masks[:, k:k + 1500], r.masks), k
+        assert np.array_equal(mid.probabilities[k:k + 1500], r.probabilities), k
     big = m.apply(np.tile(x, (40, 1)).astype(np.float64))
     for k in range(0, 60000, 7500):
         assert np.array_equal(big.masks[:, k:k + 1500], r.masks), k
